@@ -1,0 +1,778 @@
+// C ABI (include/ddmgnn_b200.h): context management, the preconditioner apply
+// pipeline and the device-resident PCG driver.
+//
+// Apply pipeline (hybrid.py:112-136), all stream-ordered on the device:
+//   for each constant-bank chunk c of ceil(k_bar / lmax):
+//       D2D copy of the chunk's fp32 weights into the __constant__ bank
+//       gnn_kernel<d, global-scratch variant>  (subdomains too large for SMEM)
+//       gnn_kernel<d, SMEM variant>            (the rest; LPT order)
+//   coarse_gemv_kernel (two-level only)
+//   prolong_kernel
+// PCG (sparse.py:76-127): one iteration = spmv_pq, update, [apply], pupdate,
+// captured once into a CUDA graph and replayed in chunks; every kernel becomes a
+// no-op once the device status word leaves "running", and the host polls the
+// status once per chunk.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/ddmgnn_b200.h"
+#include "ddmgnn_internal.h"
+
+using namespace ddmgnn;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                     \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      return fail(kCudaError, std::string("CUDA error: ") + cudaGetErrorString(_e) + " (" + \
+                                  #expr + ")");                                            \
+  } while (0)
+
+template <typename T>
+static cudaError_t dalloc(T** p, size_t count) {
+  if (*p) {
+    cudaFree(*p);
+    *p = nullptr;
+  }
+  if (count == 0) return cudaSuccess;
+  return cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * count);
+}
+template <typename T>
+static void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+struct ddmgnn_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  // matrix
+  int n = 0;
+  long long nnz = 0;
+  int *d_rowptr = nullptr, *d_col = nullptr;
+  double* d_val = nullptr;
+  // inputs kept on the host until build
+  std::vector<double> coords;
+  std::vector<int64_t> sub_ptr, sub_idx;
+  int K = 0;
+  long long batch_cap = 100000;
+  // device layout
+  bool built = false;
+  DeviceLayout lay;
+  // model
+  bool have_model = false;
+  PackedModel model;
+  float* d_bank = nullptr;
+  int n_big = 0, k_max_big = 0, k_max_small = 0;
+  // coarse
+  int coarse_k = 0;
+  double* d_cinv = nullptr;
+  // apply scratch
+  double *d_r0r = nullptr, *d_scale = nullptr, *d_zloc = nullptr, *d_y = nullptr;
+  float *d_hbuf = nullptr, *d_cbuf = nullptr, *d_qbuf = nullptr;
+  int *d_bad = nullptr, *d_outbad = nullptr, *d_status = nullptr;
+  double *d_rin = nullptr, *d_zout = nullptr;  // host-pointer apply staging
+  // pcg
+  double *d_b = nullptr, *d_u = nullptr, *d_r = nullptr, *d_p = nullptr, *d_q = nullptr,
+         *d_z = nullptr, *d_partials = nullptr, *d_hist = nullptr;
+  int hist_cap = 0;
+  PcgState* d_st = nullptr;
+  PcgState* h_st = nullptr;  // pinned
+  double *h_pin_a = nullptr, *h_pin_b = nullptr;  // pinned staging (n doubles each)
+  cudaGraphExec_t graph_exec[3] = {nullptr, nullptr, nullptr};
+};
+
+extern "C" const char* ddmgnn_last_error(void) { return g_err.c_str(); }
+extern "C" int ddmgnn_version(void) { return 1; }
+
+extern "C" int ddmgnn_create(int device, ddmgnn_ctx** out) {
+  if (!out) return fail(kValueError, "null output pointer");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(kCudaError, std::string("no CUDA device available: ") + cudaGetErrorString(e));
+  if (device < 0 || device >= ndev) return fail(kValueError, "device ordinal out of range");
+  CUDA_TRY(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(kCudaError, "ddmgnn_b200 is built for sm_100a; device " + std::string(prop.name) +
+                                " has compute capability " + std::to_string(prop.major) + "." +
+                                std::to_string(prop.minor));
+  CUDA_TRY(gnn_configure_device());
+  auto* c = new ddmgnn_ctx();
+  c->device = device;
+  e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(kCudaError, cudaGetErrorString(e));
+  }
+  e = cudaMallocHost(reinterpret_cast<void**>(&c->h_st), sizeof(PcgState));
+  if (e != cudaSuccess) {
+    cudaStreamDestroy(c->stream);
+    delete c;
+    return fail(kCudaError, cudaGetErrorString(e));
+  }
+  *out = c;
+  return kOk;
+}
+
+static void free_graphs(ddmgnn_ctx* c) {
+  for (auto& g : c->graph_exec) {
+    if (g) cudaGraphExecDestroy(g);
+    g = nullptr;
+  }
+}
+
+static void free_layout(ddmgnn_ctx* c) {
+  DeviceLayout& L = c->lay;
+  dfree(L.sub_ptr); dfree(L.idx); dfree(L.order); dfree(L.slice_base); dfree(L.slice_off);
+  dfree(L.deg); dfree(L.edges); dfree(L.tptr); dfree(L.tent); dfree(L.pou);
+  dfree(c->d_r0r); dfree(c->d_scale); dfree(c->d_zloc); dfree(c->d_y);
+  dfree(c->d_bad); dfree(c->d_outbad);
+  dfree(c->d_hbuf); dfree(c->d_cbuf); dfree(c->d_qbuf);
+  c->built = false;
+  free_graphs(c);
+}
+
+extern "C" void ddmgnn_destroy(ddmgnn_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  free_layout(c);
+  dfree(c->d_rowptr); dfree(c->d_col); dfree(c->d_val);
+  dfree(c->d_bank); dfree(c->d_cinv); dfree(c->d_status);
+  dfree(c->d_rin); dfree(c->d_zout);
+  dfree(c->d_b); dfree(c->d_u); dfree(c->d_r); dfree(c->d_p); dfree(c->d_q); dfree(c->d_z);
+  dfree(c->d_partials); dfree(c->d_hist); dfree(c->d_st);
+  if (c->h_st) cudaFreeHost(c->h_st);
+  if (c->h_pin_a) cudaFreeHost(c->h_pin_a);
+  if (c->h_pin_b) cudaFreeHost(c->h_pin_b);
+  cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+extern "C" void* ddmgnn_stream(ddmgnn_ctx* c) { return c ? c->stream : nullptr; }
+
+static cudaStream_t pick(ddmgnn_ctx* c, void* s) {
+  return s ? reinterpret_cast<cudaStream_t>(s) : c->stream;
+}
+
+extern "C" int ddmgnn_set_matrix(ddmgnn_ctx* c, int64_t n, int64_t nnz, const int64_t* indptr,
+                                 const int32_t* indices, const double* data) {
+  if (!c) return fail(kValueError, "null context");
+  if (n <= 0 || n >= (1ll << 31) || nnz < 0 || nnz >= (1ll << 31))
+    return fail(kValueError, "matrix dimensions out of range");
+  if (indptr[0] != 0 || indptr[n] != nnz) return fail(kValueError, "malformed indptr");
+  for (int64_t i = 0; i < n; ++i) {
+    if (indptr[i + 1] < indptr[i]) return fail(kValueError, "indptr not nondecreasing");
+    for (int64_t t = indptr[i]; t < indptr[i + 1]; ++t) {
+      if (indices[t] < 0 || indices[t] >= n || (t > indptr[i] && indices[t] <= indices[t - 1]))
+        return fail(kValueError,
+                    "row " + std::to_string(i) + ": columns not strictly increasing in range");
+    }
+  }
+  CUDA_TRY(cudaSetDevice(c->device));
+  if (c->n != n) free_layout(c);
+  c->n = static_cast<int>(n);
+  c->nnz = nnz;
+  std::vector<int> rp(n + 1);
+  for (int64_t i = 0; i <= n; ++i) rp[i] = static_cast<int>(indptr[i]);
+  CUDA_TRY(dalloc(&c->d_rowptr, n + 1));
+  CUDA_TRY(dalloc(&c->d_col, std::max<int64_t>(nnz, 1)));
+  CUDA_TRY(dalloc(&c->d_val, std::max<int64_t>(nnz, 1)));
+  CUDA_TRY(cudaMemcpy(c->d_rowptr, rp.data(), sizeof(int) * (n + 1), cudaMemcpyHostToDevice));
+  if (nnz) {
+    CUDA_TRY(cudaMemcpy(c->d_col, indices, sizeof(int) * nnz, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(c->d_val, data, sizeof(double) * nnz, cudaMemcpyHostToDevice));
+  }
+  // Krylov vectors
+  CUDA_TRY(dalloc(&c->d_b, n)); CUDA_TRY(dalloc(&c->d_u, n)); CUDA_TRY(dalloc(&c->d_r, n));
+  CUDA_TRY(dalloc(&c->d_p, n)); CUDA_TRY(dalloc(&c->d_q, n)); CUDA_TRY(dalloc(&c->d_z, n));
+  CUDA_TRY(dalloc(&c->d_rin, n)); CUDA_TRY(dalloc(&c->d_zout, n));
+  const int pblocks = std::max((static_cast<int>(n) + 255) / 256, 148 * 8) + 1;
+  CUDA_TRY(dalloc(&c->d_partials, 2ull * pblocks));
+  if (!c->d_st) {
+    CUDA_TRY(cudaMalloc(&c->d_st, sizeof(PcgState)));
+    CUDA_TRY(cudaMemset(c->d_st, 0, sizeof(PcgState)));
+  }
+  if (!c->d_status) {
+    CUDA_TRY(cudaMalloc(&c->d_status, sizeof(int)));
+    CUDA_TRY(cudaMemset(c->d_status, 0, sizeof(int)));
+  }
+  if (c->h_pin_a) cudaFreeHost(c->h_pin_a);
+  if (c->h_pin_b) cudaFreeHost(c->h_pin_b);
+  c->h_pin_a = c->h_pin_b = nullptr;
+  CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&c->h_pin_a), sizeof(double) * n));
+  CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&c->h_pin_b), sizeof(double) * n));
+  free_graphs(c);
+  return kOk;
+}
+
+extern "C" int ddmgnn_set_geometry(ddmgnn_ctx* c, int64_t n, const double* coords) {
+  if (!c) return fail(kValueError, "null context");
+  if (c->n && n != c->n) return fail(kValueError, "expected coords of shape (" + std::to_string(c->n) + ", 2)");
+  c->coords.assign(coords, coords + 2 * n);
+  c->built = false;
+  return kOk;
+}
+
+extern "C" int ddmgnn_set_decomposition(ddmgnn_ctx* c, int64_t k, const int64_t* sub_ptr,
+                                        const int64_t* sub_idx) {
+  if (!c) return fail(kValueError, "null context");
+  if (k <= 0 || k >= (1ll << 31)) return fail(kValueError, "number of subdomains out of range");
+  c->K = static_cast<int>(k);
+  c->sub_ptr.assign(sub_ptr, sub_ptr + k + 1);
+  c->sub_idx.assign(sub_idx, sub_idx + sub_ptr[k]);
+  c->built = false;
+  return kOk;
+}
+
+extern "C" int ddmgnn_set_batch_cap(ddmgnn_ctx* c, int64_t cap) {
+  if (!c) return fail(kValueError, "null context");
+  if (cap < 1) return fail(kValueError, "batch node cap must be >= 1");
+  c->batch_cap = cap;
+  return kOk;
+}
+
+static int refresh_classes(ddmgnn_ctx* c);
+
+extern "C" int ddmgnn_set_model(ddmgnn_ctx* c, int k_bar, int d, double alpha,
+                                const double* params, int64_t n_params) {
+  if (!c) return fail(kValueError, "null context");
+  std::string err;
+  PackedModel m;
+  int st = pack_model(k_bar, d, alpha, params, n_params, &m, &err);
+  if (st) return fail(st, err);
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(dalloc(&c->d_bank, m.bank.size()));
+  CUDA_TRY(cudaMemcpy(c->d_bank, m.bank.data(), sizeof(float) * m.bank.size(),
+                      cudaMemcpyHostToDevice));
+  const bool dim_changed = !c->have_model || c->model.d != d || c->model.k_bar != k_bar;
+  c->model = std::move(m);
+  c->have_model = true;
+  free_graphs(c);
+  if (c->built && dim_changed) return refresh_classes(c);
+  return kOk;
+}
+
+extern "C" int ddmgnn_set_coarse_inverse(ddmgnn_ctx* c, int64_t k, const double* inv) {
+  if (!c) return fail(kValueError, "null context");
+  if (c->K && k != c->K) return fail(kValueError, "coarse size must equal the number of subdomains");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(dalloc(&c->d_cinv, static_cast<size_t>(k) * k));
+  CUDA_TRY(cudaMemcpy(c->d_cinv, inv, sizeof(double) * k * k, cudaMemcpyHostToDevice));
+  c->coarse_k = static_cast<int>(k);
+  free_graphs(c);
+  return kOk;
+}
+
+template <typename T>
+static cudaError_t upload(T** dst, const std::vector<T>& v) {
+  cudaError_t e = dalloc(dst, std::max<size_t>(v.size(), 1));
+  if (e != cudaSuccess) return e;
+  if (v.empty()) return cudaSuccess;
+  return cudaMemcpy(*dst, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice);
+}
+
+// Split subdomains into the SMEM class and the global-scratch class for the
+// current latent dimension and (re)allocate the chunk scratch.
+static int refresh_classes(ddmgnn_ctx* c) {
+  if (!c->built || !c->have_model) return kOk;
+  const int cap = gnn_smem_max_nodes(c->model.d);
+  const auto& ord = c->lay.h_order;
+  const auto& sp = c->lay.h_sub_ptr;
+  int nb = 0;
+  while (nb < c->K && sp[ord[nb] + 1] - sp[ord[nb]] > cap) ++nb;
+  c->n_big = nb;
+  c->k_max_big = nb ? sp[ord[0] + 1] - sp[ord[0]] : 0;
+  c->k_max_small = nb < c->K ? sp[ord[nb] + 1] - sp[ord[nb]] : 0;
+  const int d = c->model.d;
+  const int hs = (d % 2 == 0) ? d : d + 1;
+  const int qs = (2 * d + 3) / 4 * 4;
+  const size_t V = c->lay.V;
+  const bool multi = c->model.n_chunks() > 1;
+  CUDA_TRY(dalloc(&c->d_hbuf, (multi || nb) ? V * hs : 0));
+  CUDA_TRY(dalloc(&c->d_cbuf, (multi || nb) ? V : 0));
+  CUDA_TRY(dalloc(&c->d_qbuf, nb ? V * qs : 0));
+  return kOk;
+}
+
+extern "C" int ddmgnn_build(ddmgnn_ctx* c) {
+  if (!c) return fail(kValueError, "null context");
+  if (!c->n) return fail(kStateError, "set_matrix must be called before build");
+  if (c->coords.size() != 2ull * c->n)
+    return fail(kValueError, "expected coords of shape (" + std::to_string(c->n) + ", 2)");
+  if (!c->K) return fail(kStateError, "set_decomposition must be called before build");
+  CUDA_TRY(cudaSetDevice(c->device));
+  // host copy of the CSR structure for the builder
+  std::vector<int> rp(c->n + 1);
+  CUDA_TRY(cudaMemcpy(rp.data(), c->d_rowptr, sizeof(int) * (c->n + 1), cudaMemcpyDeviceToHost));
+  std::vector<int64_t> rp64(rp.begin(), rp.end());
+  std::vector<int32_t> col(std::max<long long>(c->nnz, 1));
+  if (c->nnz)
+    CUDA_TRY(cudaMemcpy(col.data(), c->d_col, sizeof(int) * c->nnz, cudaMemcpyDeviceToHost));
+  HostLayout H;
+  std::string err;
+  int st = build_host_layout(c->n, rp64.data(), col.data(), c->coords.data(), c->K,
+                             c->sub_ptr.data(), c->sub_idx.data(), &H, &err);
+  if (st) return fail(st, err);
+  free_layout(c);
+  DeviceLayout& L = c->lay;
+  L.n = H.n; L.K = H.K; L.V = H.V; L.S = H.S; L.k_max = H.k_max; L.E = H.E; L.E_pad = H.E_pad;
+  CUDA_TRY(upload(&L.sub_ptr, H.sub_ptr));
+  CUDA_TRY(upload(&L.idx, H.idx));
+  CUDA_TRY(upload(&L.order, H.order));
+  CUDA_TRY(upload(&L.slice_base, H.slice_base));
+  CUDA_TRY(upload(&L.slice_off, H.slice_off));
+  CUDA_TRY(upload(&L.deg, H.deg));
+  CUDA_TRY(dalloc(&L.edges, std::max<long long>(H.E_pad, 1)));
+  if (H.E_pad)
+    CUDA_TRY(cudaMemcpy(L.edges, H.edges.data(), sizeof(float) * H.edges.size(),
+                        cudaMemcpyHostToDevice));
+  CUDA_TRY(upload(&L.tptr, H.tptr));
+  CUDA_TRY(dalloc(&L.tent, std::max(H.V, 1)));
+  CUDA_TRY(cudaMemcpy(L.tent, H.tent.data(), sizeof(int) * H.tent.size(), cudaMemcpyHostToDevice));
+  CUDA_TRY(upload(&L.pou, H.pou));
+  L.h_sub_ptr = H.sub_ptr;
+  L.h_order = H.order;
+  CUDA_TRY(dalloc(&c->d_r0r, c->K)); CUDA_TRY(dalloc(&c->d_scale, c->K));
+  CUDA_TRY(dalloc(&c->d_y, c->K)); CUDA_TRY(dalloc(&c->d_zloc, std::max(H.V, 1)));
+  CUDA_TRY(dalloc(&c->d_bad, c->K)); CUDA_TRY(dalloc(&c->d_outbad, c->K));
+  CUDA_TRY(cudaMemset(c->d_scale, 0, sizeof(double) * c->K));
+  c->built = true;
+  return refresh_classes(c);
+}
+
+extern "C" int ddmgnn_info(ddmgnn_ctx* c, int64_t* out, int n_out) {
+  if (!c) return fail(kValueError, "null context");
+  int64_t v[12] = {c->n, c->K, c->lay.V, c->lay.E, c->lay.E_pad, c->lay.k_max, c->lay.S,
+                   c->model.k_bar, c->model.d, c->model.lmax, c->model.n_chunks(), c->n_big};
+  for (int i = 0; i < n_out && i < 12; ++i) out[i] = v[i];
+  return kOk;
+}
+
+extern "C" int ddmgnn_export_local_graph(ddmgnn_ctx* c, int64_t sub, int64_t* n_edges,
+                                         int32_t* src, int32_t* dst, float* vec3) {
+  if (!c || !c->built) return fail(kStateError, "build must be called first");
+  if (sub < 0 || sub >= c->K) return fail(kValueError, "subdomain out of range");
+  const DeviceLayout& L = c->lay;
+  const int b = L.h_sub_ptr[sub], k = L.h_sub_ptr[sub + 1] - b;
+  std::vector<uint16_t> deg(std::max(k, 1));
+  if (k) CUDA_TRY(cudaMemcpy(deg.data(), L.deg + b, sizeof(uint16_t) * k, cudaMemcpyDeviceToHost));
+  int64_t ne = 0;
+  for (int a = 0; a < k; ++a) ne += deg[a];
+  *n_edges = ne;
+  if (!src) return kOk;
+  int sb = 0;
+  CUDA_TRY(cudaMemcpy(&sb, L.slice_base + sub, sizeof(int), cudaMemcpyDeviceToHost));
+  const int ns = (k + 31) / 32;
+  std::vector<int> so(ns + 1);
+  CUDA_TRY(cudaMemcpy(so.data(), L.slice_off + sb, sizeof(int) * (ns + 1), cudaMemcpyDeviceToHost));
+  std::vector<float4> rec(std::max(so[ns] - so[0], 1));
+  if (so[ns] > so[0])
+    CUDA_TRY(cudaMemcpy(rec.data(), L.edges + so[0], sizeof(float4) * (so[ns] - so[0]),
+                        cudaMemcpyDeviceToHost));
+  int64_t o = 0;
+  for (int a = 0; a < k; ++a) {
+    for (int e = 0; e < deg[a]; ++e) {
+      const float4 r = rec[so[a >> 5] - so[0] + 32 * e + (a & 31)];
+      src[o] = a;
+      int t;
+      std::memcpy(&t, &r.w, 4);
+      dst[o] = t;
+      vec3[3 * o] = r.x;
+      vec3[3 * o + 1] = r.y;
+      vec3[3 * o + 2] = r.z;
+      ++o;
+    }
+  }
+  return kOk;
+}
+
+static int ready(ddmgnn_ctx* c, int level) {
+  if (!c) return fail(kValueError, "null context");
+  if (level == DDMGNN_PRECOND_NONE) return c->n ? kOk : fail(kStateError, "no matrix set");
+  if (level != DDMGNN_LEVEL_ONE && level != DDMGNN_LEVEL_TWO)
+    return fail(kValueError, "level must be 1 (one-level) or 2 (two-level)");
+  if (!c->built) return fail(kStateError, "build must be called before apply");
+  if (!c->have_model) return fail(kStateError, "set_model must be called before apply");
+  if (level == DDMGNN_LEVEL_TWO && c->coarse_k != c->K)
+    return fail(kStateError, "two-level apply needs set_coarse_inverse");
+  return kOk;
+}
+
+// Enqueue restriction + GNN chunks.  status/skip: apply error word and PCG skip word.
+static cudaError_t enqueue_gnn(ddmgnn_ctx* c, const double* r, int* status, const int* skip,
+                               cudaStream_t s) {
+  const DeviceLayout& L = c->lay;
+  const PackedModel& M = c->model;
+  GnnArgs a{};
+  a.sub_ptr = L.sub_ptr; a.idx = L.idx; a.order = L.order; a.slice_base = L.slice_base;
+  a.slice_off = L.slice_off; a.deg = L.deg; a.edges = L.edges; a.pou = L.pou;
+  a.r = r; a.r0r = c->d_r0r; a.scale = c->d_scale; a.zloc = c->d_zloc;
+  a.hbuf = c->d_hbuf; a.cbuf = c->d_cbuf; a.qbuf = c->d_qbuf;
+  a.bad_layer = c->d_bad; a.out_bad = c->d_outbad; a.status = status; a.skip = skip;
+  a.alpha = M.alpha;
+  const int nch = M.n_chunks();
+  for (int ch = 0; ch < nch; ++ch) {
+    cudaError_t e = upload_bank(M.d, c->d_bank + static_cast<size_t>(ch) * kConstFloats, s);
+    if (e != cudaSuccess) return e;
+    a.first = ch == 0;
+    a.last = ch == nch - 1;
+    a.layer0 = ch * M.lmax + 1;
+    a.nl = std::min(M.lmax, M.k_bar - ch * M.lmax);
+    if (c->n_big) {
+      a.order_begin = 0;
+      e = launch_gnn(M.d, false, c->n_big, c->k_max_big, a, s);
+      if (e != cudaSuccess) return e;
+    }
+    if (c->K - c->n_big) {
+      a.order_begin = c->n_big;
+      e = launch_gnn(M.d, true, c->K - c->n_big, c->k_max_small, a, s);
+      if (e != cudaSuccess) return e;
+    }
+  }
+  return cudaSuccess;
+}
+
+// Full apply: z = M r.  mode 1 = PCG (fused <r,z>, beta).
+static cudaError_t enqueue_apply(ddmgnn_ctx* c, const double* r, double* z, int level,
+                                 int* status, const int* skip, int mode, cudaStream_t s) {
+  cudaError_t e = enqueue_gnn(c, r, status, skip, s);
+  if (e != cudaSuccess) return e;
+  if (level == DDMGNN_LEVEL_TWO) {
+    e = launch_coarse_gemv(c->K, c->d_cinv, c->d_r0r, c->d_y, skip, s);
+    if (e != cudaSuccess) return e;
+  }
+  return launch_prolong(c->n, level == DDMGNN_LEVEL_TWO, c->lay.tptr, c->lay.tent, c->lay.pou,
+                        c->d_y, c->d_scale, c->d_zloc, z, r, c->d_partials, c->d_st, mode, skip,
+                        s);
+}
+
+// Reproduce the reference's error precedence (hybrid.py:121-131, dss.py:324-325):
+// batches of loaded subdomains in order; within a batch a latent error (smallest
+// layer) wins over an output error (smallest subdomain).
+static int report_apply_error(ddmgnn_ctx* c) {
+  const int K = c->K;
+  std::vector<int> bad(K), outbad(K);
+  std::vector<double> scale(K);
+  CUDA_TRY(cudaMemcpy(bad.data(), c->d_bad, sizeof(int) * K, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(outbad.data(), c->d_outbad, sizeof(int) * K, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(scale.data(), c->d_scale, sizeof(double) * K, cudaMemcpyDeviceToHost));
+  const auto& sp = c->lay.h_sub_ptr;
+  std::vector<int> loaded;
+  for (int i = 0; i < K; ++i)
+    if (scale[i] != 0.0) loaded.push_back(i);
+  size_t pos = 0;
+  while (pos < loaded.size()) {
+    size_t end = pos;
+    long long load = 0;
+    while (end < loaded.size()) {  // plan_batches, hybrid.py:49-68
+      const long long cnt = sp[loaded[end] + 1] - sp[loaded[end]];
+      if (end > pos && load + cnt > c->batch_cap) break;
+      load += cnt;
+      ++end;
+    }
+    int min_layer = 0;
+    for (size_t t = pos; t < end; ++t) {
+      const int b = bad[loaded[t]];
+      if (b && (!min_layer || b < min_layer)) min_layer = b;
+    }
+    if (min_layer)
+      return fail(kRuntimeError, "non-finite latent state at message-passing iteration " +
+                                     std::to_string(min_layer));
+    for (size_t t = pos; t < end; ++t)
+      if (outbad[loaded[t]])
+        return fail(kRuntimeError,
+                    "non-finite model output in subdomain " + std::to_string(loaded[t]));
+    pos = end;
+  }
+  return fail(kRuntimeError, "non-finite model state (unlocated)");
+}
+
+static int check_status_word(ddmgnn_ctx* c, cudaStream_t s) {
+  int st = 0;
+  CUDA_TRY(cudaMemcpyAsync(&c->h_st->pad, c->d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  st = c->h_st->pad;
+  if (st != 0) {
+    CUDA_TRY(cudaMemsetAsync(c->d_status, 0, sizeof(int), s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return report_apply_error(c);
+  }
+  return kOk;
+}
+
+extern "C" int ddmgnn_apply(ddmgnn_ctx* c, const double* r, double* z, int level, void* stream,
+                            int check) {
+  int st = ready(c, level);
+  if (st) return st;
+  if (level == DDMGNN_PRECOND_NONE) return fail(kValueError, "level must be 1 or 2");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t s = pick(c, stream);
+  if (check) CUDA_TRY(cudaMemsetAsync(c->d_status, 0, sizeof(int), s));
+  CUDA_TRY(enqueue_apply(c, r, z, level, c->d_status, nullptr, 0, s));
+  if (check) return check_status_word(c, s);
+  return kOk;
+}
+
+extern "C" int ddmgnn_apply_host(ddmgnn_ctx* c, const double* r, double* z, int level) {
+  int st = ready(c, level);
+  if (st) return st;
+  if (level == DDMGNN_PRECOND_NONE) return fail(kValueError, "level must be 1 or 2");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  const size_t bytes = sizeof(double) * c->n;
+  std::memcpy(c->h_pin_a, r, bytes);
+  CUDA_TRY(cudaMemcpyAsync(c->d_rin, c->h_pin_a, bytes, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemsetAsync(c->d_status, 0, sizeof(int), s));
+  CUDA_TRY(enqueue_apply(c, c->d_rin, c->d_zout, level, c->d_status, nullptr, 0, s));
+  CUDA_TRY(cudaMemcpyAsync(c->h_pin_b, c->d_zout, bytes, cudaMemcpyDeviceToHost, s));
+  st = check_status_word(c, s);
+  if (st) return st;
+  std::memcpy(z, c->h_pin_b, bytes);
+  return kOk;
+}
+
+extern "C" int ddmgnn_launch_gnn_only(ddmgnn_ctx* c, const double* r, void* stream) {
+  int st = ready(c, DDMGNN_LEVEL_ONE);
+  if (st) return st;
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(enqueue_gnn(c, r, c->d_status, nullptr, pick(c, stream)));
+  return kOk;
+}
+
+extern "C" int ddmgnn_spmv(ddmgnn_ctx* c, const double* x, double* y, void* stream) {
+  if (!c || !c->n) return fail(kStateError, "no matrix set");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(launch_spmv(c->n, c->d_rowptr, c->d_col, c->d_val, x, y, pick(c, stream)));
+  return kOk;
+}
+
+// ------------------------------------------------------------------ PCG
+
+// One PCG iteration (sparse.py:106-126) as stream work; level 0 = CG.
+static cudaError_t enqueue_iteration(ddmgnn_ctx* c, int level, cudaStream_t s) {
+  const int n = c->n;
+  int* sw = &c->d_st->status;
+  cudaError_t e = launch_spmv_pq(n, c->d_rowptr, c->d_col, c->d_val, c->d_p, c->d_q,
+                                 c->d_partials, c->d_st, s);
+  if (e != cudaSuccess) return e;
+  e = launch_update(n, c->d_u, c->d_r, c->d_p, c->d_q, c->d_partials, c->d_st, c->d_hist,
+                    level == DDMGNN_PRECOND_NONE, s);
+  if (e != cudaSuccess) return e;
+  if (level != DDMGNN_PRECOND_NONE) {
+    e = enqueue_apply(c, c->d_r, c->d_z, level, sw, sw, 1, s);
+    if (e != cudaSuccess) return e;
+  }
+  return launch_pupdate(n, c->d_p, level == DDMGNN_PRECOND_NONE ? c->d_r : c->d_z, c->d_st, s);
+}
+
+static int get_graph(ddmgnn_ctx* c, int level, cudaGraphExec_t* out) {
+  if (!c->graph_exec[level]) {
+    cudaGraph_t g;
+    CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    cudaError_t e = enqueue_iteration(c, level, c->stream);
+    cudaError_t e2 = cudaStreamEndCapture(c->stream, &g);
+    if (e != cudaSuccess) return fail(kCudaError, std::string("graph capture: ") + cudaGetErrorString(e));
+    if (e2 != cudaSuccess) return fail(kCudaError, std::string("graph capture: ") + cudaGetErrorString(e2));
+    e = cudaGraphInstantiate(&c->graph_exec[level], g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(kCudaError, std::string("graph instantiate: ") + cudaGetErrorString(e));
+  }
+  *out = c->graph_exec[level];
+  return kOk;
+}
+
+static int ensure_hist(ddmgnn_ctx* c, int max_iter) {
+  if (c->hist_cap < max_iter + 1) {
+    CUDA_TRY(dalloc(&c->d_hist, max_iter + 1));
+    c->hist_cap = max_iter + 1;
+  }
+  return kOk;
+}
+
+// Common PCG prologue: u, r, ||b||, hist[0].  Returns 1 in *early if the solve ends
+// before the first iteration (sparse.py:92-99).
+static int pcg_prologue(ddmgnn_ctx* c, const double* b, const double* u0, int device_ptrs,
+                        double tol, int max_iter, cudaStream_t s, int* early, int* iterations,
+                        double* history, int* converged, double* u_out) {
+  const int n = c->n;
+  const size_t bytes = sizeof(double) * n;
+  const cudaMemcpyKind kin = device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  int st = ensure_hist(c, max_iter);
+  if (st) return st;
+  PcgState init{};
+  init.tol = tol;
+  init.max_iter = max_iter;
+  *c->h_st = init;
+  CUDA_TRY(cudaMemcpyAsync(c->d_st, c->h_st, sizeof(PcgState), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(c->d_b, b, bytes, kin, s));
+  if (u0) {
+    CUDA_TRY(cudaMemcpyAsync(c->d_u, u0, bytes, kin, s));
+    CUDA_TRY(launch_spmv(n, c->d_rowptr, c->d_col, c->d_val, c->d_u, c->d_q, s));
+    CUDA_TRY(launch_pcg_init_u0(n, c->d_b, c->d_q, c->d_r, c->d_partials, c->d_st, c->d_hist, s));
+  } else {
+    CUDA_TRY(cudaMemsetAsync(c->d_u, 0, bytes, s));
+    CUDA_TRY(launch_pcg_init(n, c->d_b, c->d_r, c->d_partials, c->d_st, c->d_hist, s));
+  }
+  CUDA_TRY(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+  double h0 = 0.0;
+  CUDA_TRY(cudaMemcpyAsync(&c->h_pin_a[0], c->d_hist, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  h0 = c->h_pin_a[0];
+  *early = 0;
+  const cudaMemcpyKind kout = device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  if (c->h_st->nb == 0.0) {  // sparse.py:93-94
+    CUDA_TRY(cudaMemsetAsync(c->d_u, 0, bytes, s));
+    CUDA_TRY(cudaMemcpyAsync(u_out, c->d_u, bytes, kout, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    *iterations = 0;
+    history[0] = 0.0;
+    *converged = 1;
+    *early = 1;
+    return kOk;
+  }
+  if (h0 < tol) {  // sparse.py:98-99
+    CUDA_TRY(cudaMemcpyAsync(u_out, c->d_u, bytes, kout, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    *iterations = 0;
+    history[0] = h0;
+    *converged = 1;
+    *early = 1;
+  }
+  return kOk;
+}
+
+static int pcg_epilogue(ddmgnn_ctx* c, int device_ptrs, cudaStream_t s, double* u_out,
+                        int* iterations, double* history, int* converged) {
+  const size_t bytes = sizeof(double) * c->n;
+  CUDA_TRY(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  const PcgState st = *c->h_st;
+  if (st.status == kNotSpd) return fail(kRuntimeError, "matrix not SPD: <p, Ap> <= 0");
+  if (st.status == kNonFiniteResidual)
+    return fail(kRuntimeError, "non-finite residual at iteration " + std::to_string(st.iter + 1));
+  CUDA_TRY(cudaMemcpyAsync(u_out, c->d_u, bytes,
+                           device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(history, c->d_hist, sizeof(double) * (st.iter + 1),
+                           cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  *iterations = st.iter;
+  *converged = st.status == kConverged;
+  return kOk;
+}
+
+extern "C" int ddmgnn_pcg(ddmgnn_ctx* c, const double* b, const double* u0, double* u, double tol,
+                          int max_iter, int level, int device_ptrs, void* stream, int* iterations,
+                          double* history, int* converged) {
+  int st = ready(c, level);
+  if (st) return st;
+  if (!(tol > 0)) return fail(kValueError, "tol must be positive");
+  if (max_iter < 0) return fail(kValueError, "max_iter must be >= 0");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t s = pick(c, stream);
+  int early = 0;
+  st = pcg_prologue(c, b, u0, device_ptrs, tol, max_iter, s, &early, iterations, history,
+                    converged, u);
+  if (st || early) return st;
+  const int n = c->n;
+  // z0 = M r0, p0 = z0, rho0 = <r0, z0>  (sparse.py:101-103)
+  if (level == DDMGNN_PRECOND_NONE) {
+    CUDA_TRY(launch_rz_init(n, c->d_r, c->d_r, c->d_p, c->d_partials, c->d_st, s));
+  } else {
+    CUDA_TRY(cudaMemsetAsync(c->d_status, 0, sizeof(int), s));
+    CUDA_TRY(enqueue_apply(c, c->d_r, c->d_z, level, c->d_status, nullptr, 0, s));
+    st = check_status_word(c, s);
+    if (st) return st;
+    CUDA_TRY(launch_rz_init(n, c->d_r, c->d_z, c->d_p, c->d_partials, c->d_st, s));
+  }
+  if (max_iter > 0) {
+    cudaGraphExec_t gx;
+    st = get_graph(c, level, &gx);
+    if (st) return st;
+    int done = 0, chunk = 2;
+    while (!done) {
+      for (int t = 0; t < chunk; ++t) CUDA_TRY(cudaGraphLaunch(gx, s));
+      CUDA_TRY(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+      done = c->h_st->status != kRunning;
+      chunk = std::min(chunk * 2, 16);
+    }
+    if (c->h_st->status == kPrecondError) {
+      // the device stopped at the failing apply; rerun it unskipped for the exact message
+      CUDA_TRY(cudaMemsetAsync(c->d_status, 0, sizeof(int), s));
+      CUDA_TRY(enqueue_apply(c, c->d_r, c->d_z, level, c->d_status, nullptr, 0, s));
+      st = check_status_word(c, s);
+      return st ? st : fail(kRuntimeError, "non-finite model state");
+    }
+  } else {
+    c->h_st->status = kMaxIter;
+    CUDA_TRY(cudaMemcpyAsync(&c->d_st->status, &c->h_st->status, sizeof(int),
+                             cudaMemcpyHostToDevice, s));
+  }
+  return pcg_epilogue(c, device_ptrs, s, u, iterations, history, converged);
+}
+
+extern "C" int ddmgnn_pcg_host_precond(ddmgnn_ctx* c, const double* b, const double* u0,
+                                       double* u, double tol, int max_iter,
+                                       ddmgnn_host_precond_fn fn, void* user, int* iterations,
+                                       double* history, int* converged) {
+  int st = ready(c, DDMGNN_PRECOND_NONE);
+  if (st) return st;
+  if (!(tol > 0)) return fail(kValueError, "tol must be positive");
+  if (!fn) return fail(kValueError, "null preconditioner callback");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  int early = 0;
+  st = pcg_prologue(c, b, u0, 0, tol, max_iter, s, &early, iterations, history, converged, u);
+  if (st || early) return st;
+  const int n = c->n;
+  const size_t bytes = sizeof(double) * n;
+  std::vector<double> rh(n), zh(n);
+  auto host_apply = [&]() -> int {
+    CUDA_TRY(cudaMemcpyAsync(rh.data(), c->d_r, bytes, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (fn(user, rh.data(), zh.data(), n) != 0)
+      return fail(kRuntimeError, "preconditioner callback failed");
+    CUDA_TRY(cudaMemcpyAsync(c->d_z, zh.data(), bytes, cudaMemcpyHostToDevice, s));
+    return kOk;
+  };
+  st = host_apply();
+  if (st) return st;
+  CUDA_TRY(launch_rz_init(n, c->d_r, c->d_z, c->d_p, c->d_partials, c->d_st, s));
+  if (max_iter == 0) {
+    c->h_st->status = kMaxIter;
+    CUDA_TRY(cudaMemcpyAsync(&c->d_st->status, &c->h_st->status, sizeof(int),
+                             cudaMemcpyHostToDevice, s));
+  }
+  for (int it = 0; it < max_iter; ++it) {
+    CUDA_TRY(launch_spmv_pq(n, c->d_rowptr, c->d_col, c->d_val, c->d_p, c->d_q, c->d_partials,
+                            c->d_st, s));
+    CUDA_TRY(launch_update(n, c->d_u, c->d_r, c->d_p, c->d_q, c->d_partials, c->d_st, c->d_hist,
+                           0, s));
+    CUDA_TRY(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (c->h_st->status != kRunning) break;
+    st = host_apply();
+    if (st) return st;
+    // rho' = <r, z>, beta, p = z + beta p via the prolong-free path
+    CUDA_TRY(launch_rz_beta(n, c->d_r, c->d_z, c->d_partials, c->d_st, s));
+    CUDA_TRY(launch_pupdate(n, c->d_p, c->d_z, c->d_st, s));
+  }
+  return pcg_epilogue(c, 0, s, u, iterations, history, converged);
+}

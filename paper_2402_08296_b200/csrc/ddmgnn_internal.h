@@ -1,0 +1,164 @@
+// Internal declarations shared by the DDM-GNN B200 library translation units.
+//
+// Device data layout (all resident in HBM, built once per preconditioner):
+//
+//   K subdomains, V = sum_i k_i batched subdomain nodes, N global DOFs.
+//   sub_ptr[K+1]  int32  batched offset of subdomain i (ascending i)
+//   idx[V]        int32  global DOF of every batched node (ascending per subdomain,
+//                        the reference's local node order, decomp.py:215)
+//   Local graphs in SELL-32 ("sliced ELL", slice = 32 consecutive local nodes =
+//   one warp): slice q of subdomain i holds w_q = max degree in the slice; record
+//   (e, lane) of the slice lives at edges[slice_off[slice_base[i]+q] + 32*e + lane].
+//   A record is float4 {dx, dy, |d|, bits(dst_local)}: the reference's edge_vec /
+//   edge_len (dss.py:184-185, computed in fp64 then rounded to fp32) and the local
+//   destination.  Records of one node are in ascending dst order, i.e. the
+//   reference's lexsorted (src, dst) edge order (dss.py:181).
+//   deg[V]        uint16 out-degree of every batched node
+//   tptr[N+1], tent[V] (int2: batched position, subdomain) — transpose map used
+//                 by the gather-based prolongation, ascending subdomain per DOF
+//                 (the reference's gluing order, hybrid.py:133-135)
+//   pou[N]        fp64   1/multiplicity  (decomp.py:184-189)
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace ddmgnn {
+
+enum Status : int {
+  kOk = 0,
+  kValueError = 1,    // Python ValueError
+  kRuntimeError = 2,  // Python RuntimeError
+  kCudaError = 3,
+  kStateError = 4,    // API misuse (missing set_* call)
+};
+
+// PCG / apply device status word values
+enum DevStatus : int {
+  kRunning = 0,
+  kConverged = 1,
+  kMaxIter = 2,
+  kNotSpd = 3,
+  kNonFiniteResidual = 4,
+  kPrecondError = 5,
+};
+
+constexpr int kGnnThreads = 512;
+constexpr int kConstFloats = 16384;  // 64 KB constant bank
+
+struct DeviceLayout {
+  int n = 0, K = 0, V = 0, S = 0, k_max = 0;
+  long long E = 0, E_pad = 0;
+  int *sub_ptr = nullptr, *idx = nullptr, *order = nullptr;
+  int *slice_base = nullptr, *slice_off = nullptr;
+  uint16_t* deg = nullptr;
+  float4* edges = nullptr;
+  int* tptr = nullptr;
+  int2* tent = nullptr;
+  double* pou = nullptr;
+  std::vector<int> h_sub_ptr;  // host copies of the small arrays
+  std::vector<int> h_order;    // LPT order (descending k, ascending id)
+};
+
+struct HostLayout {
+  int n = 0, K = 0, V = 0, S = 0, k_max = 0;
+  long long E = 0, E_pad = 0;
+  std::vector<int> sub_ptr, idx, order, slice_base, slice_off;
+  std::vector<uint16_t> deg;
+  std::vector<float> edges;  // 4 floats per record
+  std::vector<int> tptr;
+  std::vector<int> tent;  // 2 ints per entry
+  std::vector<double> pou;
+};
+
+// layout.cpp
+int build_host_layout(int n, const int64_t* indptr, const int32_t* indices, const double* coords,
+                      int K, const int64_t* sub_ptr, const int64_t* sub_idx, HostLayout* out,
+                      std::string* err);
+
+// model packing (layout.cpp)
+struct PackedModel {
+  int k_bar = 0, d = 0, lmax = 0, stride = 0, dec_off = 0;
+  float alpha = 0.f;
+  std::vector<float> bank;  // n_chunks * 16384 floats: chunk c = layers [c*lmax, ...)
+  int n_chunks() const { return lmax ? (k_bar + lmax - 1) / lmax : 0; }
+};
+int gnn_supported_dim(int d);
+int gnn_lmax(int d);
+int gnn_stride(int d);
+int gnn_smem_node_bytes(int d);
+int pack_model(int k_bar, int d, double alpha, const double* params, long long n_params,
+               PackedModel* out, std::string* err);
+
+// kernels (gnn.cu)
+struct GnnArgs {
+  const int* sub_ptr;
+  const int* idx;
+  const int* order;
+  const int* slice_base;
+  const int* slice_off;
+  const uint16_t* deg;
+  const float4* edges;
+  const double* pou;
+  const double* r;
+  double* r0r;
+  double* scale;
+  double* zloc;
+  float* hbuf;  // V * HS  (multi-chunk models)
+  float* cbuf;  // V       (multi-chunk models)
+  float* qbuf;  // V * QS  (global-memory variant)
+  int* bad_layer;
+  int* out_bad;
+  int* status;       // apply error word (atomicMax kPrecondError)
+  const int* skip;   // PCG status word: kernels are no-ops when *skip != 0 (may be null)
+  float alpha;
+  int layer0;        // 1-based index of the first layer of this chunk
+  int nl;            // layers in this chunk
+  int first, last;   // chunk flags
+  int order_begin;   // CTA b handles subdomain order[order_begin + b]
+};
+int gnn_smem_max_nodes(int d);
+// WSRC WDST WE B1 W2O B2O W2I B2I WP1 BP1 WP2 BP2 STRIDE D2P DP DEC_W1 DEC_B1 DEC_W2 DEC_B2 LMAX
+int gnn_bank_offsets(int d, int* o);
+cudaError_t gnn_configure_device();
+cudaError_t upload_bank(int d, const float* dev_bank, cudaStream_t s);  // D2D into the constant bank
+cudaError_t launch_gnn(int d, bool smem_variant, int n_ctas, int k_max, const GnnArgs& a,
+                       cudaStream_t s);
+
+// krylov.cu
+struct PcgState {
+  double rho, pq, alpha, beta, rr, nb, rz, tol;
+  int iter, max_iter, status, pad;
+  unsigned int tickets[8];
+};
+constexpr int kRedThreads = 256;
+int reduce_blocks(int n);
+cudaError_t launch_coarse_gemv(int K, const double* inv, const double* x, double* y,
+                               const int* skip, cudaStream_t s);
+cudaError_t launch_prolong(int n, int two_level, const int* tptr, const int2* tent,
+                           const double* pou, const double* y, const double* scale,
+                           const double* zloc, double* z, const double* r, double* partials,
+                           PcgState* st, int mode, const int* skip, cudaStream_t s);
+cudaError_t launch_spmv(int n, const int* rowptr, const int* col, const double* val,
+                        const double* x, double* y, cudaStream_t s);
+cudaError_t launch_spmv_pq(int n, const int* rowptr, const int* col, const double* val,
+                           const double* p, double* q, double* partials, PcgState* st,
+                           cudaStream_t s);
+cudaError_t launch_update(int n, double* u, double* r, const double* p, const double* q,
+                          double* partials, PcgState* st, double* hist, int identity_precond,
+                          cudaStream_t s);
+cudaError_t launch_pupdate(int n, double* p, const double* z, PcgState* st, cudaStream_t s);
+cudaError_t launch_pcg_init(int n, const double* b, double* r, double* partials, PcgState* st,
+                            double* hist, cudaStream_t s);
+cudaError_t launch_rz_init(int n, const double* r, const double* z, double* p, double* partials,
+                           PcgState* st, cudaStream_t s);
+cudaError_t launch_copy(int n, const double* src, double* dst, cudaStream_t s);
+cudaError_t launch_rz_beta(int n, const double* r, const double* z, double* partials,
+                           PcgState* st, cudaStream_t s);
+cudaError_t launch_pcg_init_u0(int n, const double* b, const double* au0, double* r,
+                               double* partials, PcgState* st, double* hist, cudaStream_t s);
+
+}  // namespace ddmgnn

@@ -1,0 +1,47 @@
+// One latent dimension of the fused GNN kernel per translation unit (compiled
+// with -DGNN_D=<d>): each unit owns its own 64 KB constant bank, and the units
+// compile in parallel.
+#include "ddmgnn_internal.h"
+
+#ifndef GNN_D
+#error "compile with -DGNN_D=<latent dimension>"
+#endif
+
+namespace ddmgnn {
+static __constant__ float c_w[kConstFloats];
+}
+
+#include "gnn_impl.cuh"
+
+#define DDM_CAT2(a, b) a##b
+#define DDM_CAT(a, b) DDM_CAT2(a, b)
+
+namespace ddmgnn {
+
+template <bool SV>
+static cudaError_t launch_one(int n_ctas, int k_max, const GnnArgs& a, cudaStream_t s) {
+  const size_t smem = SV ? static_cast<size_t>(k_max) * Cfg<GNN_D>::SMEM_NODE_BYTES : 0;
+  int threads = ((k_max + 31) / 32) * 32;
+  if (threads > kGnnThreads) threads = kGnnThreads;
+  if (threads < 64) threads = 64;
+  gnn_kernel<GNN_D, SV><<<n_ctas, threads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t DDM_CAT(gnn_configure_d, GNN_D)() {
+  return cudaFuncSetAttribute(gnn_kernel<GNN_D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              227 * 1024 - 1024);
+}
+
+cudaError_t DDM_CAT(gnn_upload_d, GNN_D)(const float* dev_bank, cudaStream_t s) {
+  return cudaMemcpyToSymbolAsync(c_w, dev_bank, sizeof(float) * kConstFloats, 0,
+                                 cudaMemcpyDeviceToDevice, s);
+}
+
+cudaError_t DDM_CAT(gnn_launch_d, GNN_D)(bool smem_variant, int n_ctas, int k_max,
+                                         const GnnArgs& a, cudaStream_t s) {
+  return smem_variant ? launch_one<true>(n_ctas, k_max, a, s)
+                      : launch_one<false>(n_ctas, k_max, a, s);
+}
+
+}  // namespace ddmgnn

@@ -1,0 +1,386 @@
+// Krylov-loop and gluing kernels for sm_100a (all fp64, HBM-bound).
+//
+// Replaces, per PCG iteration of pkg/src/ddmgnn/sparse.py:76-127:
+//   q = A p (:107) + <p, q> (:108) + alpha (:111)          -> spmv_pq_kernel
+//   u += alpha p, r -= alpha q (:112-113) + ||r|| (:114)    -> update_kernel
+//   p = z + beta p (:126)                                   -> pupdate_kernel
+// and the two-level gluing of hybrid.py:117,133-135:
+//   y = (R0 A R0^T)^-1 (R0 r)        -> coarse_gemv_kernel (dense inverse, fp64)
+//   z_j = sum_{i ∋ j, asc} pou_j y_i + sum_{i ∋ j, asc} s_i sol_i[j]
+//                                    -> prolong_kernel (gather over the transpose map,
+//                                       fused with <r, z> for rho, sparse.py:123)
+// Elementwise updates use explicit __dmul_rn/__dadd_rn so they round exactly like
+// numpy (no FMA contraction); the per-DOF gluing and the SpMV row sums run in the
+// reference's sequential order, so given equal inputs they are bit-identical to
+// scipy.  Dot products use a deterministic two-stage tree reduction (fixed grid,
+// fixed order), which differs from BLAS ddot only by summation order.
+#include <cmath>
+
+#include "ddmgnn_internal.h"
+
+namespace ddmgnn {
+
+constexpr int kMaxRedBlocks = 148 * 8;
+
+int reduce_blocks(int n) {
+  int b = (n + kRedThreads - 1) / kRedThreads;
+  if (b > kMaxRedBlocks) b = kMaxRedBlocks;
+  return b < 1 ? 1 : b;
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum; result valid in thread 0.  blockDim.x must be a multiple of 32.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV]) {
+  __shared__ double sh[NV][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int t = 0; t < NV; ++t) v[t] = warp_sum_d(v[t]);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int t = 0; t < NV; ++t) sh[t][warp] = v[t];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int t = 0; t < NV; ++t) {
+      double x = lane < nw ? sh[t][lane] : 0.0;
+      v[t] = warp_sum_d(x);
+    }
+  }
+}
+
+// Deterministic grid reduction: every block deposits its partial; the last block to
+// arrive sums all partials in block order.  Returns true in thread 0 of that block,
+// with the totals in v.
+template <int NV>
+__device__ bool grid_sum(double (&v)[NV], double* partials, unsigned int* ticket) {
+  __shared__ bool am_last;
+  block_sum<NV>(v);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int t = 0; t < NV; ++t) partials[static_cast<size_t>(blockIdx.x) * NV + t] = v[t];
+    __threadfence();
+    const unsigned int prev = atomicAdd(ticket, 1u);
+    am_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last) return false;
+  __threadfence();
+  double acc[NV];
+#pragma unroll
+  for (int t = 0; t < NV; ++t) acc[t] = 0.0;
+  for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += blockDim.x) {
+#pragma unroll
+    for (int t = 0; t < NV; ++t) acc[t] += __ldcg(&partials[static_cast<size_t>(b) * NV + t]);
+  }
+  block_sum<NV>(acc);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int t = 0; t < NV; ++t) v[t] = acc[t];
+    *ticket = 0u;
+    return true;
+  }
+  return false;
+}
+
+// ------------------------------------------------------------------ SpMV
+// CSR SpMV, one row per thread, the block's nonzeros staged through SMEM with
+// coalesced loads; each row is summed sequentially in column order (scipy
+// csr_matvec order).
+constexpr int kSpmvRows = 256;
+constexpr int kSpmvStage = 3072;
+
+template <bool PQ>
+__global__ void __launch_bounds__(kSpmvRows) spmv_kernel(int n, const int* __restrict__ rowptr,
+                                                         const int* __restrict__ col,
+                                                         const double* __restrict__ val,
+                                                         const double* __restrict__ x,
+                                                         double* __restrict__ y, double* partials,
+                                                         PcgState* st) {
+  if (PQ && st->status != kRunning) return;
+  __shared__ int s_col[kSpmvStage];
+  __shared__ double s_val[kSpmvStage];
+  const int r0 = blockIdx.x * kSpmvRows;
+  const int r1 = min(n, r0 + kSpmvRows);
+  const int row = r0 + threadIdx.x;
+  const int e0 = rowptr[r0], e1 = rowptr[r1];
+  const bool staged = (e1 - e0) <= kSpmvStage;
+  if (staged) {
+    for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+      s_col[e - e0] = col[e];
+      s_val[e - e0] = val[e];
+    }
+  }
+  __syncthreads();
+  double acc = 0.0, pq = 0.0;
+  if (row < r1) {
+    const int b = rowptr[row], e = rowptr[row + 1];
+    if (staged) {
+      for (int t = b; t < e; ++t)
+        acc = __dadd_rn(acc, __dmul_rn(s_val[t - e0], __ldg(&x[s_col[t - e0]])));
+    } else {
+      for (int t = b; t < e; ++t) acc = __dadd_rn(acc, __dmul_rn(val[t], __ldg(&x[col[t]])));
+    }
+    y[row] = acc;
+    if (PQ) pq = x[row] * acc;
+  }
+  if (PQ) {
+    double v[1] = {pq};
+    if (grid_sum<1>(v, partials, &st->tickets[0])) {
+      st->pq = v[0];
+      if (v[0] <= 0.0) {  // sparse.py:109-110
+        st->status = kNotSpd;
+      } else {
+        st->alpha = st->rho / v[0];  // sparse.py:111
+      }
+    }
+  }
+}
+
+cudaError_t launch_spmv(int n, const int* rowptr, const int* col, const double* val,
+                        const double* x, double* y, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  spmv_kernel<false><<<(n + kSpmvRows - 1) / kSpmvRows, kSpmvRows, 0, s>>>(
+      n, rowptr, col, val, x, y, nullptr, nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spmv_pq(int n, const int* rowptr, const int* col, const double* val,
+                           const double* p, double* q, double* partials, PcgState* st,
+                           cudaStream_t s) {
+  spmv_kernel<true><<<(n + kSpmvRows - 1) / kSpmvRows, kSpmvRows, 0, s>>>(
+      n, rowptr, col, val, p, q, partials, st);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ BLAS-1
+__global__ void __launch_bounds__(kRedThreads) update_kernel(int n, double* __restrict__ u,
+                                                             double* __restrict__ r,
+                                                             const double* __restrict__ p,
+                                                             const double* __restrict__ q,
+                                                             double* partials, PcgState* st,
+                                                             double* hist, int identity) {
+  if (st->status != kRunning) return;
+  const double alpha = st->alpha;
+  double rr = 0.0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    u[j] = __dadd_rn(u[j], __dmul_rn(alpha, p[j]));  // sparse.py:112
+    const double rj = __dsub_rn(r[j], __dmul_rn(alpha, q[j]));  // sparse.py:113
+    r[j] = rj;
+    rr += rj * rj;
+  }
+  double v[1] = {rr};
+  if (grid_sum<1>(v, partials, &st->tickets[1])) {
+    const double rel = sqrt(v[0]) / st->nb;  // sparse.py:114
+    st->rr = v[0];
+    if (!isfinite(rel)) {  // sparse.py:115-116
+      st->status = kNonFiniteResidual;
+      return;
+    }
+    const int it = st->iter + 1;
+    hist[it] = rel;  // sparse.py:117
+    st->iter = it;
+    if (rel < st->tol) {  // sparse.py:119-121
+      st->status = kConverged;
+    } else if (it >= st->max_iter) {
+      st->status = kMaxIter;
+    } else if (identity) {  // plain CG: z = r, rho' = r.r (sparse.py:122-125)
+      st->beta = v[0] / st->rho;
+      st->rho = v[0];
+    }
+  }
+}
+
+cudaError_t launch_update(int n, double* u, double* r, const double* p, const double* q,
+                          double* partials, PcgState* st, double* hist, int identity_precond,
+                          cudaStream_t s) {
+  update_kernel<<<reduce_blocks(n), kRedThreads, 0, s>>>(n, u, r, p, q, partials, st, hist,
+                                                         identity_precond);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(kRedThreads) pupdate_kernel(int n, double* __restrict__ p,
+                                                              const double* __restrict__ z,
+                                                              const PcgState* st) {
+  if (st->status != kRunning) return;
+  const double beta = st->beta;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    p[j] = __dadd_rn(z[j], __dmul_rn(beta, p[j]));  // sparse.py:126
+}
+
+cudaError_t launch_pupdate(int n, double* p, const double* z, PcgState* st, cudaStream_t s) {
+  pupdate_kernel<<<reduce_blocks(n), kRedThreads, 0, s>>>(n, p, z, st);
+  return cudaGetLastError();
+}
+
+// r = b - A u0 (Au0 may be null for u0 = 0), ||b||, hist[0] (sparse.py:92-97)
+__global__ void __launch_bounds__(kRedThreads) init_kernel(int n, const double* __restrict__ b,
+                                                           const double* __restrict__ au0,
+                                                           double* __restrict__ r,
+                                                           double* partials, PcgState* st,
+                                                           double* hist) {
+  double bb = 0.0, rr = 0.0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const double bj = b[j];
+    const double rj = au0 ? __dsub_rn(bj, au0[j]) : bj;
+    r[j] = rj;
+    bb += bj * bj;
+    rr += rj * rj;
+  }
+  double v[2] = {bb, rr};
+  if (grid_sum<2>(v, partials, &st->tickets[2])) {
+    const double nb = sqrt(v[0]);
+    st->nb = nb;
+    st->rr = v[1];
+    st->iter = 0;
+    hist[0] = nb == 0.0 ? 0.0 : sqrt(v[1]) / nb;
+  }
+}
+
+cudaError_t launch_pcg_init(int n, const double* b, double* r, double* partials, PcgState* st,
+                            double* hist, cudaStream_t s) {
+  // r may already hold A u0 (then it is read as au0 and overwritten in place)
+  init_kernel<<<reduce_blocks(n), kRedThreads, 0, s>>>(n, b, nullptr, r, partials, st, hist);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pcg_init_u0(int n, const double* b, const double* au0, double* r,
+                               double* partials, PcgState* st, double* hist, cudaStream_t s) {
+  init_kernel<<<reduce_blocks(n), kRedThreads, 0, s>>>(n, b, au0, r, partials, st, hist);
+  return cudaGetLastError();
+}
+
+// p = z, rho = <r, z>  (sparse.py:102-103)
+__global__ void __launch_bounds__(kRedThreads) rz_init_kernel(int n, const double* __restrict__ r,
+                                                              const double* __restrict__ z,
+                                                              double* __restrict__ p,
+                                                              double* partials, PcgState* st) {
+  double rz = 0.0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const double zj = z[j];
+    p[j] = zj;
+    rz += r[j] * zj;
+  }
+  double v[1] = {rz};
+  if (grid_sum<1>(v, partials, &st->tickets[3])) {
+    st->rho = v[0];
+    st->rz = v[0];
+  }
+}
+
+cudaError_t launch_rz_init(int n, const double* r, const double* z, double* p, double* partials,
+                           PcgState* st, cudaStream_t s) {
+  rz_init_kernel<<<reduce_blocks(n), kRedThreads, 0, s>>>(n, r, z, p, partials, st);
+  return cudaGetLastError();
+}
+
+// rho' = <r, z>, beta = rho'/rho, rho = rho'  (sparse.py:123-125), for host-side
+// preconditioner callbacks
+__global__ void __launch_bounds__(kRedThreads) rz_beta_kernel(int n, const double* __restrict__ r,
+                                                              const double* __restrict__ z,
+                                                              double* partials, PcgState* st) {
+  if (st->status != kRunning) return;
+  double rz = 0.0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    rz += r[j] * z[j];
+  double v[1] = {rz};
+  if (grid_sum<1>(v, partials, &st->tickets[5])) {
+    st->rz = v[0];
+    st->beta = v[0] / st->rho;
+    st->rho = v[0];
+  }
+}
+
+cudaError_t launch_rz_beta(int n, const double* r, const double* z, double* partials,
+                           PcgState* st, cudaStream_t s) {
+  rz_beta_kernel<<<reduce_blocks(n), kRedThreads, 0, s>>>(n, r, z, partials, st);
+  return cudaGetLastError();
+}
+
+__global__ void copy_kernel(int n, const double* __restrict__ a, double* __restrict__ b) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    b[j] = a[j];
+}
+
+cudaError_t launch_copy(int n, const double* src, double* dst, cudaStream_t s) {
+  copy_kernel<<<reduce_blocks(n), kRedThreads, 0, s>>>(n, src, dst);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ coarse level
+// y = inv(R0 A R0^T) x, warp per row (fp64, row-major inverse).  Replaces the
+// dense LU solve of sparse.py:163 (coarse matrix factorised at setup).
+__global__ void __launch_bounds__(256) coarse_gemv_kernel(int K, const double* __restrict__ inv,
+                                                          const double* __restrict__ x,
+                                                          double* __restrict__ y,
+                                                          const int* skip) {
+  if (skip != nullptr && *skip != kRunning) return;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= K) return;
+  const double* row = inv + static_cast<size_t>(warp) * K;
+  double acc = 0.0;
+  for (int j = lane; j < K; j += 32) acc = fma(__ldg(&row[j]), __ldg(&x[j]), acc);
+  acc = warp_sum_d(acc);
+  if (lane == 0) y[warp] = acc;
+}
+
+cudaError_t launch_coarse_gemv(int K, const double* inv, const double* x, double* y,
+                               const int* skip, cudaStream_t s) {
+  const int blocks = (K * 32 + 255) / 256;
+  coarse_gemv_kernel<<<blocks, 256, 0, s>>>(K, inv, x, y, skip);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ prolongation
+// mode 0: plain apply.  mode 1: PCG — also <r, z> -> rho', beta (sparse.py:123-125).
+__global__ void __launch_bounds__(kRedThreads) prolong_kernel(
+    int n, int two_level, const int* __restrict__ tptr, const int2* __restrict__ tent,
+    const double* __restrict__ pou, const double* __restrict__ y,
+    const double* __restrict__ scale, const double* __restrict__ zloc, double* __restrict__ z,
+    const double* __restrict__ r, double* partials, PcgState* st, int mode,
+    const int* skip) {
+  if (skip != nullptr && *skip != kRunning) return;
+  double rz = 0.0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const int b = tptr[j], e = tptr[j + 1];
+    double acc = 0.0;
+    if (two_level) {  // z = r0.T @ y  (CSC matvec order: ascending subdomain)
+      const double w = pou[j];
+      for (int t = b; t < e; ++t) acc = __dadd_rn(acc, __dmul_rn(w, y[tent[t].y]));
+    }
+    for (int t = b; t < e; ++t) {  // z[idx_i] += s_i * sol_i, ascending i (hybrid.py:134-135)
+      const int2 pe = tent[t];
+      if (scale[pe.y] != 0.0) acc = __dadd_rn(acc, zloc[pe.x]);
+    }
+    z[j] = acc;
+    if (mode == 1) rz += r[j] * acc;
+  }
+  if (mode == 1) {
+    double v[1] = {rz};
+    if (grid_sum<1>(v, partials, &st->tickets[4])) {
+      st->rz = v[0];
+      st->beta = v[0] / st->rho;  // sparse.py:124
+      st->rho = v[0];
+    }
+  }
+}
+
+cudaError_t launch_prolong(int n, int two_level, const int* tptr, const int2* tent,
+                           const double* pou, const double* y, const double* scale,
+                           const double* zloc, double* z, const double* r, double* partials,
+                           PcgState* st, int mode, const int* skip, cudaStream_t s) {
+  prolong_kernel<<<reduce_blocks(n), kRedThreads, 0, s>>>(n, two_level, tptr, tent, pou, y,
+                                                          scale, zloc, z, r, partials, st, mode,
+                                                          skip);
+  return cudaGetLastError();
+}
+
+}  // namespace ddmgnn

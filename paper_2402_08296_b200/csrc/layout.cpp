@@ -1,0 +1,303 @@
+// Host-side (setup-time) builders: batched subdomain graph layout and the
+// constant-bank weight packing.
+//
+// build_host_layout replaces the reference's per-subdomain template
+// construction — build_local_graphs (pkg/src/ddmgnn/hybrid.py:36-46) =
+// extract_local_matrix (asm.py:28-32, A[idx][:, idx]) + local_graph_from_matrix
+// (dss.py:173-186) — and the partition-of-unity bookkeeping of
+// _finish_decomposition (decomp.py:180-193) with one O(V + E) pass in C++,
+// parallel over subdomains (OpenMP).  Edges are the structural off-diagonal
+// pattern of A restricted to the subdomain, both directions, in ascending
+// (src, dst) local order — exactly the reference's lexsort order because local
+// node order is ascending global DOF order.
+#include <omp.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "ddmgnn_internal.h"
+
+namespace ddmgnn {
+
+int build_host_layout(int n, const int64_t* indptr, const int32_t* indices, const double* coords,
+                      int K, const int64_t* sub_ptr, const int64_t* sub_idx, HostLayout* out,
+                      std::string* err) {
+  HostLayout& L = *out;
+  if (K <= 0) {
+    *err = "decomposition has no subdomains";
+    return kValueError;
+  }
+  const long long V64 = sub_ptr[K];
+  if (V64 >= (1ll << 31)) {
+    *err = "total subdomain size exceeds 2^31";
+    return kValueError;
+  }
+  L.n = n;
+  L.K = K;
+  L.V = static_cast<int>(V64);
+  L.sub_ptr.resize(K + 1);
+  L.idx.resize(L.V);
+  std::vector<double> mult(n, 0.0);
+  int k_max = 0;
+  for (int i = 0; i < K; ++i) {
+    const long long b = sub_ptr[i], e = sub_ptr[i + 1];
+    if (e < b) {
+      *err = "sub_ptr must be nondecreasing";
+      return kValueError;
+    }
+    L.sub_ptr[i] = static_cast<int>(b);
+    if (e - b > k_max) k_max = static_cast<int>(e - b);
+    for (long long p = b; p < e; ++p) {
+      const long long g = sub_idx[p];
+      if (g < 0 || g >= n) {
+        *err = "subdomain index out of range";
+        return kValueError;
+      }
+      if (p > b && g <= sub_idx[p - 1]) {
+        *err = "subdomain index arrays must be strictly ascending";
+        return kValueError;
+      }
+      L.idx[p] = static_cast<int>(g);
+      mult[g] += 1.0;  // decomp.py:186-187
+    }
+  }
+  L.sub_ptr[K] = L.V;
+  L.k_max = k_max;
+  for (int j = 0; j < n; ++j) {
+    if (mult[j] == 0.0) {
+      *err = "subdomains do not cover all DOFs";  // decomp.py:188-189
+      return kValueError;
+    }
+  }
+  L.pou.resize(n);
+  for (int j = 0; j < n; ++j) L.pou[j] = 1.0 / mult[j];  // decomp.py:190
+
+  // ---- pass 1: local out-degree of every batched node ----
+  L.deg.assign(L.V, 0);
+  int deg_overflow = 0;
+#pragma omp parallel
+  {
+    std::vector<int> loc(n, -1);
+#pragma omp for schedule(dynamic, 4)
+    for (int i = 0; i < K; ++i) {
+      const int b = L.sub_ptr[i], e = L.sub_ptr[i + 1];
+      for (int p = b; p < e; ++p) loc[L.idx[p]] = p - b;
+      for (int p = b; p < e; ++p) {
+        const int g = L.idx[p];
+        int cnt = 0;
+        for (long long jj = indptr[g]; jj < indptr[g + 1]; ++jj) {
+          const int c = indices[jj];
+          if (c != g && loc[c] >= 0) ++cnt;
+        }
+        if (cnt > 65535) {
+#pragma omp atomic write
+          deg_overflow = 1;
+          cnt = 65535;
+        }
+        L.deg[p] = static_cast<uint16_t>(cnt);
+      }
+      for (int p = b; p < e; ++p) loc[L.idx[p]] = -1;
+    }
+  }
+  if (deg_overflow) {
+    *err = "local node degree exceeds 65535";
+    return kValueError;
+  }
+
+  // ---- SELL-32 slices ----
+  L.slice_base.resize(K);
+  int S = 0;
+  for (int i = 0; i < K; ++i) {
+    L.slice_base[i] = S;
+    S += (L.sub_ptr[i + 1] - L.sub_ptr[i] + 31) / 32;
+  }
+  L.S = S;
+  L.slice_off.resize(S + 1);
+  long long off = 0, E = 0;
+  for (int i = 0; i < K; ++i) {
+    const int b = L.sub_ptr[i], k = L.sub_ptr[i + 1] - b;
+    for (int q = 0; q * 32 < k; ++q) {
+      int w = 0;
+      for (int t = q * 32; t < std::min(k, q * 32 + 32); ++t) {
+        w = std::max<int>(w, L.deg[b + t]);
+        E += L.deg[b + t];
+      }
+      L.slice_off[L.slice_base[i] + q] = static_cast<int>(off);
+      off += 32ll * w;
+      if (off >= (1ll << 31)) {
+        *err = "padded edge count exceeds 2^31";
+        return kValueError;
+      }
+    }
+  }
+  L.slice_off[S] = static_cast<int>(off);
+  L.E = E;
+  L.E_pad = off;
+  L.edges.assign(static_cast<size_t>(off) * 4, 0.f);
+
+  // ---- pass 2: edge records {dx, dy, |d|, dst} (dss.py:177-185) ----
+#pragma omp parallel
+  {
+    std::vector<int> loc(n, -1);
+#pragma omp for schedule(dynamic, 4)
+    for (int i = 0; i < K; ++i) {
+      const int b = L.sub_ptr[i], e = L.sub_ptr[i + 1];
+      for (int p = b; p < e; ++p) loc[L.idx[p]] = p - b;
+      for (int p = b; p < e; ++p) {
+        const int a = p - b, g = L.idx[p];
+        const long long base = L.slice_off[L.slice_base[i] + (a >> 5)] + (a & 31);
+        int slot = 0;
+        for (long long jj = indptr[g]; jj < indptr[g + 1]; ++jj) {
+          const int c = indices[jj];
+          if (c == g || loc[c] < 0) continue;
+          const double dx = coords[2 * c] - coords[2 * g];
+          const double dy = coords[2 * c + 1] - coords[2 * g + 1];
+          const double len = std::hypot(dx, dy);
+          float* rec = &L.edges[static_cast<size_t>(base + 32ll * slot) * 4];
+          rec[0] = static_cast<float>(dx);
+          rec[1] = static_cast<float>(dy);
+          rec[2] = static_cast<float>(len);
+          int dst = loc[c];
+          std::memcpy(&rec[3], &dst, 4);
+          ++slot;
+        }
+      }
+      for (int p = b; p < e; ++p) loc[L.idx[p]] = -1;
+    }
+  }
+
+  // ---- transpose map: per DOF, (batched position, subdomain) in ascending subdomain ----
+  L.tptr.assign(n + 1, 0);
+  for (int p = 0; p < L.V; ++p) L.tptr[L.idx[p] + 1]++;
+  for (int j = 0; j < n; ++j) L.tptr[j + 1] += L.tptr[j];
+  L.tent.resize(2ull * L.V);
+  {
+    std::vector<int> cur(L.tptr.begin(), L.tptr.end() - 1);
+    for (int i = 0; i < K; ++i)
+      for (int p = L.sub_ptr[i]; p < L.sub_ptr[i + 1]; ++p) {
+        const int slot = cur[L.idx[p]]++;
+        L.tent[2ull * slot] = p;
+        L.tent[2ull * slot + 1] = i;
+      }
+  }
+
+  // ---- longest-processing-time order of subdomains (descending size) ----
+  L.order.resize(K);
+  std::iota(L.order.begin(), L.order.end(), 0);
+  std::stable_sort(L.order.begin(), L.order.end(), [&](int x, int y) {
+    return (L.sub_ptr[x + 1] - L.sub_ptr[x]) > (L.sub_ptr[y + 1] - L.sub_ptr[y]);
+  });
+  return kOk;
+}
+
+// Pack the reference's flat float64 parameters (dss.py:93-99 order: per layer
+// phi_out, phi_in, psi, dec, each (w1, b1, w2, b2)) into fp32 constant banks.
+// Per-layer bank layout (gnn_cfg.h, rows padded to 4 floats):
+//   Wsrc[D][2D] Wdst[D][2D] We[3][2D] b1cat[2D]   rows of W1cat (dss.py:281-290,
+//                                                  in-MLP dx,dy rows negated)
+//   W2o[D][D] b2o[D] W2i[D][D] b2i[D] Wp1[3D+1][D] bp1[D] Wp2[D][D] bp2[D]
+// and the FINAL layer's decoder (dss.py:327; only the last output is consumed by
+// hybrid.py:124) at the end of every bank: Wd1[D][D] bd1[D] wd2[D] bd2.
+int pack_model(int k_bar, int d, double alpha, const double* params, long long n_params,
+               PackedModel* out, std::string* err) {
+  if (k_bar < 1 || d < 1) {
+    *err = "k_bar and d must be >= 1";
+    return kValueError;
+  }
+  int o[20];
+  if (!gnn_bank_offsets(d, o)) {
+    *err = "latent dimension d=" + std::to_string(d) +
+           " has no compiled kernel (supported: 3, 4, 10)";
+    return kValueError;
+  }
+  const long long expect = static_cast<long long>(k_bar) * (11ll * d * d + 15ll * d + 1);
+  if (n_params != expect) {
+    *err = "weight block size mismatch: expected " + std::to_string(expect * 8) +
+           " bytes for k_bar=" + std::to_string(k_bar) + ", d=" + std::to_string(d) + ", got " +
+           std::to_string(n_params * 8);
+    return kValueError;
+  }
+  enum { WSRC, WDST, WE, B1, W2O, B2O, W2I, B2I, WP1, BP1, WP2, BP2, STRIDE, D2P, DP, DW1, DB1,
+         DW2, DB2, LMAX };
+  const int D = d;
+  const int lmax = o[LMAX], stride = o[STRIDE], d2p = o[D2P], dp = o[DP];
+  PackedModel& M = *out;
+  M.k_bar = k_bar;
+  M.d = d;
+  M.lmax = lmax;
+  M.stride = stride;
+  M.dec_off = o[DW1];
+  M.alpha = static_cast<float>(alpha);
+  const int nch = (k_bar + lmax - 1) / lmax;
+  M.bank.assign(static_cast<size_t>(nch) * kConstFloats, 0.f);
+
+  const double* p = params;
+  const double* last_dec = nullptr;
+  for (int l = 0; l < k_bar; ++l) {
+    const double* w1o = p; p += (2 * D + 3) * D;
+    const double* b1o = p; p += D;
+    const double* w2o = p; p += D * D;
+    const double* b2o = p; p += D;
+    const double* w1i = p; p += (2 * D + 3) * D;
+    const double* b1i = p; p += D;
+    const double* w2i = p; p += D * D;
+    const double* b2i = p; p += D;
+    const double* wp1 = p; p += (3 * D + 1) * D;
+    const double* bp1 = p; p += D;
+    const double* wp2 = p; p += D * D;
+    const double* bp2 = p; p += D;
+    last_dec = p;
+    p += D * D + D + D + 1;
+    float* B = &M.bank[static_cast<size_t>(l / lmax) * kConstFloats + (l % lmax) * stride];
+    auto w1cat = [&](int row, int j) -> double {  // (2D+3) x 2D, dss.py:288-290
+      if (j < D) return w1o[row * D + j];
+      double v = w1i[row * D + (j - D)];
+      if (row == 2 * D || row == 2 * D + 1) v = -v;
+      return v;
+    };
+    auto f = [](double v) { return static_cast<float>(v); };
+    for (int m = 0; m < D; ++m)
+      for (int j = 0; j < 2 * D; ++j) {
+        B[o[WSRC] + m * d2p + j] = f(w1cat(m, j));
+        B[o[WDST] + m * d2p + j] = f(w1cat(D + m, j));
+      }
+    for (int r = 0; r < 3; ++r)
+      for (int j = 0; j < 2 * D; ++j) B[o[WE] + r * d2p + j] = f(w1cat(2 * D + r, j));
+    for (int j = 0; j < D; ++j) {
+      B[o[B1] + j] = f(b1o[j]);
+      B[o[B1] + D + j] = f(b1i[j]);
+      B[o[B2O] + j] = f(b2o[j]);
+      B[o[B2I] + j] = f(b2i[j]);
+      B[o[BP1] + j] = f(bp1[j]);
+      B[o[BP2] + j] = f(bp2[j]);
+    }
+    for (int m = 0; m < D; ++m)
+      for (int j = 0; j < D; ++j) {
+        B[o[W2O] + m * dp + j] = f(w2o[m * D + j]);
+        B[o[W2I] + m * dp + j] = f(w2i[m * D + j]);
+        B[o[WP2] + m * dp + j] = f(wp2[m * D + j]);
+      }
+    for (int m = 0; m < 3 * D + 1; ++m)
+      for (int j = 0; j < D; ++j) B[o[WP1] + m * dp + j] = f(wp1[m * D + j]);
+  }
+  // decoder of the final layer: w1 [D][D], b1 [D], w2 [D][1], b2 [1]
+  const double* dw1 = last_dec;
+  const double* db1 = dw1 + D * D;
+  const double* dw2 = db1 + D;
+  const double* db2 = dw2 + D;
+  for (int c = 0; c < nch; ++c) {
+    float* B = &M.bank[static_cast<size_t>(c) * kConstFloats];
+    for (int m = 0; m < D; ++m)
+      for (int j = 0; j < D; ++j) B[o[DW1] + m * dp + j] = static_cast<float>(dw1[m * D + j]);
+    for (int j = 0; j < D; ++j) {
+      B[o[DB1] + j] = static_cast<float>(db1[j]);
+      B[o[DW2] + j] = static_cast<float>(dw2[j]);
+    }
+    B[o[DB2]] = static_cast<float>(db2[0]);
+  }
+  return kOk;
+}
+
+}  // namespace ddmgnn

@@ -1,0 +1,118 @@
+"""Device-resident Krylov solve: the drop-in for pkg/src/ddmgnn/sparse.py.
+
+    pcg(a, b, precond, tol, max_iter, u0=None) -> (u, SolveReport)   sparse.py:76-127
+    cg(a, b, tol, max_iter, u0=None)                                 sparse.py:130-132
+    SolveReport                                                      sparse.py:31-53
+
+The recurrence is the reference's Algorithm 1 exactly (standard PCG,
+beta = rho_{k+1}/rho_k), run on the GPU in fp64: CSR SpMV fused with <p,Ap>,
+fused axpy + norm, the preconditioner kernels, all captured in a CUDA graph.
+``precond`` may be
+  * a DdmGnnPreconditioner built on the same matrix -> fully on device;
+  * None -> plain CG on device;
+  * any other callable r -> z -> the Krylov loop stays on the device and the
+    callable is invoked on host copies of r (the reference's operator hook).
+"""
+
+from __future__ import annotations
+
+import json
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _lib
+
+__all__ = ["SolveReport", "validate_csr", "pcg", "cg"]
+
+
+@dataclass
+class SolveReport:
+    """Iteration record of one Krylov solve (sparse.py:31-53)."""
+
+    iterations: int
+    residual_history: list
+    converged: bool
+    final_relres: float
+    tolerance: float = field(default=0.0, repr=False)
+
+    def to_json(self) -> str:
+        return json.dumps({"iterations": self.iterations, "converged": self.converged,
+                           "final_relres": self.final_relres,
+                           "residual_history": self.residual_history})
+
+
+def validate_csr(a: sp.csr_matrix) -> None:
+    """CSR structural invariants (sparse.py:56-67)."""
+    n_rows, n_cols = a.shape
+    indptr, indices = a.indptr, a.indices
+    if indptr[0] != 0 or indptr[-1] != a.nnz or len(indptr) != n_rows + 1:
+        raise ValueError("malformed indptr")
+    if np.any(np.diff(indptr) < 0):
+        raise ValueError("indptr not nondecreasing")
+    d = np.diff(indices)
+    row_of = np.repeat(np.arange(n_rows), np.diff(indptr))
+    same_row = row_of[1:] == row_of[:-1]
+    bad = same_row & (d <= 0)
+    if np.any(bad) or (indices.size and (indices.min() < 0 or indices.max() >= n_cols)):
+        r = int(row_of[1:][bad][0]) if np.any(bad) else 0
+        raise ValueError(f"row {r}: columns not strictly increasing in range")
+
+
+_solver_cache: dict = {}
+
+
+def _same_matrix(a, b) -> bool:
+    if a is b:
+        return True
+    return (a.shape == b.shape and a.nnz == b.nnz and np.array_equal(a.indptr, b.indptr)
+            and np.array_equal(a.indices, b.indices) and np.array_equal(a.data, b.data))
+
+
+def _solver_ctx(a, device: int = 0) -> _lib.Context:
+    """A context holding only the matrix (plain CG / host preconditioners)."""
+    hit = _solver_cache.get(device)
+    if hit is not None and _same_matrix(hit[0], a):
+        return hit[1]
+    ctx = _lib.Context(device)
+    ctx.set_matrix(a)
+    _solver_cache[device] = (a, ctx)
+    return ctx
+
+
+def _as_csr(a):
+    a = sp.csr_matrix(a)
+    if not a.has_sorted_indices:
+        a = a.copy()
+        a.sort_indices()
+    return a
+
+
+def pcg(a, b, precond, tol: float, max_iter: int, u0=None):
+    """Preconditioned conjugate gradient on the GPU; returns (u, SolveReport)."""
+    from .hybrid import DdmGnnPreconditioner
+
+    if tol <= 0:
+        raise ValueError("tol must be positive")
+    b = np.asarray(b, dtype=float)
+    n = b.shape[0]
+    if u0 is not None:
+        u0 = np.asarray(u0, dtype=float)
+        if u0.shape != (n,):
+            raise ValueError("u0 dimension mismatch")
+    a = _as_csr(a)
+    if isinstance(precond, DdmGnnPreconditioner) and _same_matrix(precond.a, a):
+        ctx, level = precond.context, precond._level_code
+        u, it, hist, conv = ctx.pcg(b, u0, tol, max_iter, level)
+    elif precond is None:
+        u, it, hist, conv = _solver_ctx(a).pcg(b, u0, tol, max_iter, _lib.PRECOND_NONE)
+    else:
+        fn = precond if callable(precond) else precond.__call__
+        u, it, hist, conv = _solver_ctx(a).pcg_host_precond(b, u0, tol, max_iter, fn)
+    return u, SolveReport(it, hist, conv, hist[-1], tol)
+
+
+def cg(a, b, tol: float, max_iter: int, u0=None):
+    """Unpreconditioned conjugate gradient (sparse.py:130-132)."""
+    return pcg(a, b, None, tol, max_iter, u0=u0)

@@ -1,0 +1,326 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the reference's
+golden vectors and the CPU oracle.  Mirrors the hot-path tests of the
+reference suite (pkg/tests/test_hybrid.py, test_dss.py, test_sparse.py,
+test_acceptance.py) with the fp32 tolerance of the north star (1e-5 relative
+L2 on apply(r); Krylov iteration counts within +-1)."""
+import os
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from conftest import GOLDEN, load_golden, problem_from, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5  # fp32 apply parity bar (BASELINE.json north_star)
+
+
+@pytest.fixture(scope="module")
+def ddm():
+    import paper_2402_08296_b200 as m
+    from paper_2402_08296_b200 import _lib
+
+    _lib.load()
+    return m
+
+
+def _dec(ddm, g, prefix=""):
+    a, b, coords, subs = problem_from(g, prefix)
+    dec = ddm.finish_decomposition(subs, g[f"{prefix}owner"], int(g[f"{prefix}overlap"]))
+    return a, b, coords, dec
+
+
+def _golden_model(ddm, g, tag):
+    kb, d, seed = (int(x) for x in g[f"{tag}_meta"])
+    model = ddm.init_model(kb, d, alpha=float(g[f"{tag}_alpha"]), seed=seed)
+    assert np.array_equal(ddm.flat_params(model), g[f"{tag}_flat"])
+    return model
+
+
+def _desk(ddm):
+    path = os.path.join(GOLDEN, "desk_k10_d10.dss")
+    if not os.path.exists(path):
+        pytest.skip("desk weights missing")
+    return ddm.load_model(path)
+
+
+# ---------------------------------------------------------------- layout
+
+
+def test_device_templates_match_reference(ddm):
+    """Edges and edge features equal the reference templates (test_hybrid.py:22-44)."""
+    g = load_golden("small.npz")
+    a, _b, coords, dec = _dec(ddm, g)
+    p = ddm.build_ddm_gnn(a, coords, dec, _golden_model(ddm, g, "m340"))
+    offs = np.concatenate(([0], np.cumsum(g["tpl_counts"])))
+    for i in range(dec.n_subdomains):
+        t = p.local_graph(i)
+        sl = slice(offs[i], offs[i + 1])
+        assert np.array_equal(t.edges, g["tpl_edges"][sl])
+        assert np.array_equal(t.edge_vec, g["tpl_edge_vec"][sl].astype(np.float32))
+        assert np.array_equal(t.edge_len, g["tpl_edge_len"][sl].astype(np.float32))
+    info = p.info()
+    assert info["V"] == sum(s.size for s in dec.subdomains)
+    assert info["E"] == int(g["tpl_counts"].sum())
+
+
+# ---------------------------------------------------------------- apply parity
+
+
+@pytest.mark.parametrize("tag", ["m340", "m234"])
+@pytest.mark.parametrize("level", ["two", "one"])
+def test_apply_matches_reference_small(ddm, tag, level):
+    g = load_golden("small.npz")
+    a, _b, coords, dec = _dec(ddm, g)
+    p = ddm.build_ddm_gnn(a, coords, dec, _golden_model(ddm, g, tag), level=level)
+    key = f"{tag}_z_two" if level == "two" else f"{tag}_z_loc"
+    for k, r in enumerate(g["r"]):
+        z = p(r)
+        assert rel_l2(z, g[key][k]) < TOL
+
+
+def test_apply_matches_reference_config_a(ddm):
+    g = load_golden("A.npz")
+    a, _b, coords, dec = _dec(ddm, g)
+    model = ddm.init_model(10, 10, seed=1)
+    assert np.array_equal(ddm.flat_params(model), g["m1010_flat"])
+    p2 = ddm.build_ddm_gnn(a, coords, dec, model)
+    p1 = ddm.build_ddm_gnn(a, coords, dec, model, level="one")
+    assert rel_l2(p2(g["r"]), g["m1010_z_two"]) < TOL
+    # local-only term: the GNN part itself (SURVEY.md finding 5)
+    assert rel_l2(p1(g["r"]), g["m1010_z_loc"]) < TOL
+
+
+def test_apply_desk_weights_config_a(ddm):
+    g = load_golden("A.npz")
+    if "desk_z_two" not in g:
+        pytest.skip("fixture without desk weights")
+    a, _b, coords, dec = _dec(ddm, g)
+    model = _desk(ddm)
+    p2 = ddm.build_ddm_gnn(a, coords, dec, model)
+    p1 = ddm.build_ddm_gnn(a, coords, dec, model, level="one")
+    assert rel_l2(p2(g["r"]), g["desk_z_two"]) < TOL
+    assert rel_l2(p1(g["r"]), g["desk_z_loc"]) < TOL
+
+
+def test_apply_heldout_desk(ddm):
+    g = load_golden("heldout.npz")
+    model = _desk(ddm)
+    for j in range(5):
+        a, _b, coords, dec = _dec(ddm, g, f"p{j}_")
+        p2 = ddm.build_ddm_gnn(a, coords, dec, model)
+        p1 = ddm.build_ddm_gnn(a, coords, dec, model, level="one")
+        assert rel_l2(p2(g[f"p{j}_r"]), g[f"p{j}_z_two"]) < TOL
+        assert rel_l2(p1(g[f"p{j}_r"]), g[f"p{j}_z_loc"]) < TOL
+
+
+def test_multi_chunk_model_matches_oracle(ddm):
+    """k_bar=30 (three constant-bank chunks) against the oracle."""
+    from oracle import ddm_oracle as orc
+
+    g = load_golden("small.npz")
+    a, _b, coords, dec = _dec(ddm, g)
+    model = ddm.init_model(30, 10, seed=3)
+    p = ddm.build_ddm_gnn(a, coords, dec, model)
+    assert p.info()["n_chunks"] > 1
+    om = orc.model_from_flat(30, 10, model.alpha, 3, ddm.flat_params(model))
+    ref = orc.OraclePreconditioner(a, coords, dec.subdomains, om, "one")
+    p1 = ddm.build_ddm_gnn(a, coords, dec, model, level="one")
+    for r in g["r"][:2]:
+        assert rel_l2(p1(r), ref(r)) < TOL
+        assert rel_l2(p(r), orc.OraclePreconditioner(a, coords, dec.subdomains, om, "two")(r)) < TOL
+
+
+def test_large_subdomains_use_global_variant(ddm):
+    """Subdomains too large for shared memory run the global-scratch kernel."""
+    from oracle import ddm_oracle as orc
+
+    g = load_golden("A.npz")
+    a, _b, coords, dec = _dec(ddm, g)
+    merged = [np.union1d(np.union1d(dec.subdomains[0], dec.subdomains[1]), dec.subdomains[2]),
+              np.union1d(dec.subdomains[3], dec.subdomains[4])]
+    dec2 = ddm.finish_decomposition(merged, dec.base_owner, dec.overlap)
+    model = ddm.init_model(10, 10, seed=1)
+    p = ddm.build_ddm_gnn(a, coords, dec2, model, level="one")
+    assert p.info()["n_big"] >= 1
+    om = orc.model_from_flat(10, 10, model.alpha, 1, ddm.flat_params(model))
+    ref = orc.OraclePreconditioner(a, coords, merged, om, "one")
+    assert rel_l2(p(g["r"]), ref(g["r"])) < TOL
+
+
+# ---------------------------------------------------------------- invariants
+
+
+def test_positive_homogeneity(ddm):
+    """z(2r) = 2 z(r) (test_hybrid.py:55-61) — bitwise here."""
+    g = load_golden("small.npz")
+    a, _b, coords, dec = _dec(ddm, g)
+    p = ddm.build_ddm_gnn(a, coords, dec, ddm.init_model(3, 4, seed=0))
+    rng = np.random.default_rng(0)
+    for _ in range(5):
+        r = rng.standard_normal(a.shape[0])
+        z1, z2 = p(r), p(2.0 * r)
+        assert np.abs(z2 - 2.0 * z1).max() <= 1e-12 * max(np.abs(z1).max(), 1e-30)
+
+
+def test_zero_residual_is_zero(ddm):
+    g = load_golden("small.npz")
+    a, _b, coords, dec = _dec(ddm, g)
+    p = ddm.build_ddm_gnn(a, coords, dec, ddm.init_model(3, 4, seed=0))
+    assert np.all(p(np.zeros(a.shape[0])) == 0.0)
+
+
+def test_zero_subdomain_contributes_nothing(ddm):
+    """test_hybrid.py:69-87 against the oracle."""
+    from oracle import ddm_oracle as orc
+
+    g = load_golden("small.npz")
+    a, _b, coords, dec = _dec(ddm, g)
+    model = ddm.init_model(3, 4, seed=0)
+    p = ddm.build_ddm_gnn(a, coords, dec, model)
+    r = np.random.default_rng(1).standard_normal(a.shape[0])
+    r[dec.subdomains[0]] = 0.0
+    om = orc.model_from_flat(3, 4, model.alpha, 0, ddm.flat_params(model))
+    assert rel_l2(p(r), orc.OraclePreconditioner(a, coords, dec.subdomains, om)(r)) < TOL
+
+
+def test_bitwise_invariant_to_batch_cap(ddm):
+    """test_hybrid.py:101-108."""
+    g = load_golden("small.npz")
+    a, _b, coords, dec = _dec(ddm, g)
+    model = ddm.init_model(2, 3, seed=4)
+    p_big = ddm.build_ddm_gnn(a, coords, dec, model)
+    p_small = ddm.build_ddm_gnn(a, coords, dec, model, batch_nodes_cap=120)
+    r = np.random.default_rng(3).standard_normal(a.shape[0])
+    assert np.array_equal(p_big(r), p_small(r))
+
+
+def test_deterministic_repeat(ddm):
+    g = load_golden("A.npz")
+    a, _b, coords, dec = _dec(ddm, g)
+    p = ddm.build_ddm_gnn(a, coords, dec, ddm.init_model(10, 10, seed=1))
+    assert np.array_equal(p(g["r"]), p(g["r"]))
+
+
+def test_nan_output_names_subdomain(ddm):
+    """test_hybrid.py:111-120."""
+    g = load_golden("small.npz")
+    a, _b, coords, dec = _dec(ddm, g)
+    model = ddm.init_model(2, 3, seed=4)
+    model.layers[-1].dec.w2[...] = np.nan
+    p = ddm.build_ddm_gnn(a, coords, dec, model)
+    r = np.random.default_rng(5).standard_normal(a.shape[0])
+    with pytest.raises(RuntimeError, match="non-finite model output in subdomain 0"):
+        p(r)
+
+
+def test_nan_latent_names_iteration(ddm):
+    """test_dss.py:96-100 through the preconditioner."""
+    g = load_golden("small.npz")
+    a, _b, coords, dec = _dec(ddm, g)
+    model = ddm.init_model(3, 3, seed=1)
+    model.layers[1].psi.b2[...] = np.inf
+    p = ddm.build_ddm_gnn(a, coords, dec, model)
+    with pytest.raises(RuntimeError, match="non-finite latent state at message-passing iteration 2"):
+        p(np.random.default_rng(0).standard_normal(a.shape[0]))
+
+
+def test_coords_shape_checked(ddm):
+    g = load_golden("small.npz")
+    a, _b, coords, dec = _dec(ddm, g)
+    with pytest.raises(ValueError):
+        ddm.build_ddm_gnn(a, coords[:-1], dec, ddm.init_model(2, 3))
+    p = ddm.build_ddm_gnn(a, coords, dec, ddm.init_model(2, 3))
+    with pytest.raises(ValueError):
+        p(np.zeros(a.shape[0] + 1))
+
+
+def test_torch_device_tensors_zero_copy(ddm):
+    import torch
+
+    g = load_golden("A.npz")
+    a, _b, coords, dec = _dec(ddm, g)
+    p = ddm.build_ddm_gnn(a, coords, dec, ddm.init_model(10, 10, seed=1))
+    rt = torch.tensor(g["r"], device="cuda:0")
+    zt = p(rt)
+    assert zt.is_cuda and zt.dtype == torch.float64
+    assert np.array_equal(zt.cpu().numpy(), p(g["r"]))
+
+
+# ---------------------------------------------------------------- Krylov
+
+
+def test_cg_matches_reference_history(ddm):
+    g = load_golden("small.npz")
+    a, b, _c, _d = _dec(ddm, g)
+    u, rep = ddm.cg(a, b, 1e-8, 500)
+    assert rep.converged and abs(rep.iterations - int(g["cg_iters"])) <= 1
+    m = min(len(rep.residual_history), len(g["cg_hist"]))
+    assert np.allclose(rep.residual_history[:m], g["cg_hist"][:m], rtol=1e-6)
+    assert len(rep.residual_history) == rep.iterations + 1
+    assert rep.final_relres == rep.residual_history[-1] < 1e-8
+
+
+def test_cg_known_answers(ddm):
+    """test_sparse.py:24-50."""
+    a = sp.identity(17, format="csr")
+    b = np.random.default_rng(0).standard_normal(17)
+    u, rep = ddm.cg(a, b, 1e-12, 10)
+    assert rep.iterations == 1 and rep.converged and np.allclose(u, b, rtol=1e-14)
+    a = sp.csr_matrix(np.diag([1.0, 2.0, 3.0]))
+    u, rep = ddm.cg(a, np.ones(3), 1e-12, 10)
+    assert rep.converged and rep.iterations <= 3
+    assert np.allclose(u, [1.0, 0.5, 1.0 / 3.0], rtol=1e-12)
+    u, rep = ddm.cg(sp.identity(5, format="csr"), np.zeros(5), 1e-10, 10)
+    assert rep.converged and rep.iterations == 0 and np.all(u == 0.0)
+    g = load_golden("small.npz")
+    a, b, _c, _d = _dec(ddm, g)
+    _, rep = ddm.cg(a, b, 1e-12, 3)
+    assert not rep.converged and rep.iterations == 3 and len(rep.residual_history) == 4
+
+
+def test_pcg_identity_matches_cg(ddm):
+    """test_sparse.py:60-66 (host-callback preconditioner path)."""
+    g = load_golden("small.npz")
+    a, b, _c, _d = _dec(ddm, g)
+    u1, rep1 = ddm.cg(a, b, 1e-8, 500)
+    u2, rep2 = ddm.pcg(a, b, lambda r: r, 1e-8, 500)
+    assert rep1.iterations == rep2.iterations
+    assert np.abs(u1 - u2).max() <= 1e-14 * np.abs(u1).max()
+
+
+def test_pcg_rejects_indefinite(ddm):
+    a = sp.csr_matrix(np.diag([1.0, -1.0]))
+    with pytest.raises(RuntimeError, match="not SPD"):
+        ddm.pcg(a, np.ones(2), None, 1e-8, 10)
+    with pytest.raises(ValueError, match="tol must be positive"):
+        ddm.pcg(a, np.ones(2), None, 0.0, 10)
+
+
+def test_pcg_ddm_gnn_desk_heldout_iterations(ddm):
+    """Held-out acceptance problems (test_acceptance.py:170-191): +-1 iteration."""
+    g = load_golden("heldout.npz")
+    model = _desk(ddm)
+    for j in range(5):
+        a, b, coords, dec = _dec(ddm, g, f"p{j}_")
+        p = ddm.build_ddm_gnn(a, coords, dec, model)
+        u, rep = ddm.pcg(a, b, p, 1e-6, 500)
+        ref = g[f"p{j}_hist"]
+        assert rep.converged
+        assert abs(rep.iterations - (len(ref) - 1)) <= 1, (j, rep.iterations, len(ref) - 1)
+        assert rep.final_relres < 1e-6
+        res = np.linalg.norm(b - a @ u) / np.linalg.norm(b)
+        assert res < 1.01e-6
+
+
+def test_pcg_ddm_gnn_desk_config_a(ddm):
+    g = load_golden("A.npz")
+    if "desk_pcg_hist" not in g:
+        pytest.skip("fixture without desk weights")
+    a, b, coords, dec = _dec(ddm, g)
+    p = ddm.build_ddm_gnn(a, coords, dec, _desk(ddm))
+    _u, rep = ddm.pcg(a, b, p, 1e-6, 500)
+    ref = g["desk_pcg_hist"]
+    assert bool(rep.converged) == bool(g["desk_pcg_converged"])
+    assert abs(rep.iterations - (len(ref) - 1)) <= 1
