@@ -1,0 +1,385 @@
+"""Benchmark of the DDM-GNN hot path on B200.
+
+Workload (BASELINE.json configs[2], "C"): 2D Poisson P1 blob mesh with
+~1M nodes (generate_blob_mesh(0, 1_000_000, 0.2), coefficients seed (0,1)),
+partition(A, 1000, 0), overlap 2 -> N=996,546 DOFs, K=997 subdomains,
+two-level DDM-GNN (k_bar=10, d=10, random-init weights init_model(10,10,seed=1)),
+built on the box by the native problem builder (bit-identical to the reference).
+
+A "step" is one preconditioner application z = M r over the whole problem
+(restriction + batched GNN over all 997 subdomains + coarse solve + gluing).
+  value  = precond applies/sec, device-timed with CUDA events per step, inputs
+           resident in HBM, L2 flushed (256 MB write) before every step.
+  e2e    = same metric through the C ABI with HOST buffers (ddmgnn_apply_host:
+           pinned H2D of r, apply, D2H of z inside the timed region).
+Also reported: the fused GNN kernel's roofline (FP32 CUDA-core bound), the
+SpMV's HBM roofline, a full PCG solve (time per iteration / time-to-solution),
+and the CPU baseline (the oracle restatement of the reference, numpy/OpenBLAS
+on the host cores, on a bounded sample of subdomains).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "time-to-solution to 1e-6 (s) and precond applies/sec, 1/2/4/8 B200 vs host CPU"
+UNIT = "precond applies/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--target-nodes", type=int, default=1_000_000)
+    ap.add_argument("--subdomain-size", type=int, default=1000)
+    ap.add_argument("--overlap", type=int, default=2)
+    ap.add_argument("--kbar", type=int, default=10)
+    ap.add_argument("--d", type=int, default=10)
+    ap.add_argument("--level", default="two", choices=["one", "two"])
+    ap.add_argument("--weights", default="random", help="'random' or a dss-v1 file")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-pcg", action="store_true")
+    return ap.parse_args()
+
+
+def gnn_flops(k_bar, d, v, e):
+    """Minimal factorised FP32 flops of one GNN apply."""
+    per_node = (8 * d * d + 2 * d) + (4 * d * d + 4 * d) + (2 * (3 * d + 1) * d + 2 * d * d + 2 * d) + 2 * d
+    return float(k_bar * (per_node * v + 16 * d * e) + (2 * d * d + 2 * d) * v)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self._stop = threading.Event()
+        self._proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except FileNotFoundError:
+            self._proc = None
+        return self
+
+    def _read(self):
+        for line in self._proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self._proc:
+            time.sleep(0.25)
+            self._proc.terminate()
+            self._proc.wait(timeout=5)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for nm, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def build_workload(args):
+    from paper_2402_08296_b200.problem import ProblemConfig, build_problem
+
+    t0 = time.perf_counter()
+    prob = build_problem(0, ProblemConfig(args.target_nodes, 0.2, args.subdomain_size, args.overlap))
+    return prob, time.perf_counter() - t0
+
+
+def load_model(args):
+    import paper_2402_08296_b200 as ddm
+
+    if args.weights == "random":
+        return ddm.init_model(args.kbar, args.d, seed=1)
+    return ddm.load_model(args.weights)
+
+
+# ----------------------------------------------------------------------------- CPU baseline
+
+
+def cpu_baseline(prob, args, seconds):
+    """Oracle restatement of the reference apply (numpy/OpenBLAS, all host threads)
+    on a bounded sample of subdomains, extrapolated linearly in subdomain nodes."""
+    from oracle import ddm_oracle as orc
+
+    import paper_2402_08296_b200 as ddm
+
+    model = load_model(args)
+    om = orc.model_from_flat(model.k_bar, model.d, model.alpha, model.seed, ddm.flat_params(model))
+    subs = prob.dec.subdomains
+    a = prob.system.a
+    rng = np.random.default_rng(0)
+    r = rng.standard_normal(a.shape[0])
+    v_total = sum(s.size for s in subs)
+    sample, v_s = [], 0
+    # sample sized so one forward is ~1/3 of the budget at ~30 us/node
+    target_nodes = max(2000, int(seconds / 3 / 3e-5))
+    for i in range(len(subs)):
+        sample.append(i)
+        v_s += subs[i].size
+        if v_s >= target_nodes:
+            break
+    graphs = [orc.local_graph(a, subs[i], prob.coords) for i in sample]
+    cs = []
+    for i in sample:
+        ri = r[subs[i]]
+        cs.append(ri / np.linalg.norm(ri))
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        orc.forward(om, graphs, cs)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds / 3 or reps >= 3:
+            break
+    per_apply_s = el / reps * (v_total / v_s)
+    return {
+        "value": 1.0 / per_apply_s,
+        "unit": UNIT,
+        "cores": os.cpu_count(),
+        "kind": "port",
+        "sample": f"{len(sample)}/{len(subs)} subdomains ({v_s}/{v_total} subdomain nodes), "
+                  f"{reps} forward(s) of oracle/ddm_oracle.py (restatement of dss.py:302-329), "
+                  f"extrapolated linearly in subdomain nodes; restriction/coarse/gluing (<2% on the "
+                  f"reference) not included",
+        "seconds_per_apply": per_apply_s,
+    }
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    prob, _ = build_workload(args)
+    vals = []
+    for _ in range(args.warmup + args.steps if args.steps <= 2 else args.steps):
+        res = cpu_baseline(prob, args, max(3.0, args.cpu_seconds / max(1, args.steps)))
+        vals.append(res["value"])
+    v = float(np.median(vals))
+    res["value"] = v
+    out = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / v,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"C: blob mesh {args.target_nodes} nodes, N_s={args.subdomain_size}, "
+                               f"overlap {args.overlap}, {args.level}-level DDM-GNN k_bar={args.kbar} d={args.d}"},
+        "cpu_baseline": res,
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+
+    import paper_2402_08296_b200 as ddm
+
+    prob, t_setup = build_workload(args)
+    model = load_model(args)
+    t0 = time.perf_counter()
+    p = ddm.build_ddm_gnn(prob.system.a, prob.coords, prob.dec, model, level=args.level,
+                          device=local)
+    t_build = time.perf_counter() - t0
+    info = p.info()
+    ctx = p.context
+    n = prob.system.n
+    lvl = 2 if args.level == "two" else 1
+    dev = torch.device(f"cuda:{local}")
+    r = torch.tensor(np.random.default_rng(rank).standard_normal(n), device=dev)
+    z = torch.empty_like(r)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > L2
+    stream = torch.cuda.Stream(dev)  # events and kernels on the same (non-default) stream
+    torch.cuda.set_stream(stream)
+    s = stream.cuda_stream
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    # warmup (also checks the apply for non-finite states once)
+    ctx.apply_device(r.data_ptr(), z.data_ptr(), lvl, s, True)
+    for _ in range(max(0, args.warmup - 1)):
+        ctx.apply_device(r.data_ptr(), z.data_ptr(), lvl, s, False)
+    barrier()
+
+    # ---- device-timed applies (per-step events, L2 flushed outside the events) ----
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    gnn_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        barrier()
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            ctx.apply_device(r.data_ptr(), z.data_ptr(), lvl, s, False)
+            ev[i][1].record(stream)
+        barrier()
+        # the dominant kernel alone (restriction + fused GNN), same stream
+        for i in range(args.steps):
+            flush.zero_()
+            gnn_ev[i][0].record(stream)
+            ctx.launch_gnn_only(r.data_ptr(), s)
+            gnn_ev[i][1].record(stream)
+        barrier()
+    ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    gnn_ms = sum(a.elapsed_time(b) for a, b in gnn_ev) / args.steps
+    ms_t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = world * 1e3 / ms_max
+
+    # ---- SpMV roofline (HBM) ----
+    a = prob.system.a
+    x = torch.tensor(np.ones(n), device=dev)
+    y = torch.empty_like(x)
+    for _ in range(3):
+        ctx.spmv_device(x.data_ptr(), y.data_ptr(), s)
+    sp_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+    for e0, e1 in sp_ev:
+        flush.zero_()
+        e0.record(stream)
+        ctx.spmv_device(x.data_ptr(), y.data_ptr(), s)
+        e1.record(stream)
+    torch.cuda.synchronize(dev)
+    spmv_ms = sum(e0.elapsed_time(e1) for e0, e1 in sp_ev) / len(sp_ev)
+    spmv_bytes = 12 * a.nnz + 20 * n
+
+    # ---- end to end through the C ABI with host buffers ----
+    r_host = np.random.default_rng(rank).standard_normal(n)
+    for _ in range(2):
+        ctx.apply_host(r_host, lvl)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ctx.apply_host(r_host, lvl)
+    t_e2e = (time.perf_counter() - t0) / args.steps
+    e2e_t = torch.tensor([t_e2e], device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = world / float(e2e_t.item())
+
+    # ---- a full PCG solve (device-resident) ----
+    pcg = None
+    if not args.no_pcg:
+        b = prob.system.b
+        t0 = time.perf_counter()
+        u, rep = ddm.pcg(a, b, p, 1e-6, 200)
+        t_pcg = time.perf_counter() - t0
+        pcg = {"iterations": rep.iterations, "converged": rep.converged,
+               "final_relres": rep.final_relres, "seconds": t_pcg,
+               "ms_per_iteration": 1e3 * t_pcg / max(1, rep.iterations),
+               "max_iter": 200, "weights": args.weights}
+
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    fp32_peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+    flops = gnn_flops(info["k_bar"], info["d"], info["V"], info["E"])
+    achieved = flops / (gnn_ms * 1e-3) / 1e12
+    n_gnn_launches = info["n_chunks"] * (1 + (1 if info["n_big"] else 0))
+    per_step_launches = n_gnn_launches + (1 if lvl == 2 else 0) + 1
+    clocks = clk.summary()
+    if rank == 0:
+        cpu = cpu_baseline(prob, args, args.cpu_seconds) if world == 1 else None
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 GNN / f64 Krylov+gluing",
+            "data": "synthetic (reference problem generator restated natively; random-init weights)",
+            "config": {
+                "workload": f"C: blob mesh target {args.target_nodes} nodes (N={n}), "
+                            f"N_s={args.subdomain_size}, overlap {args.overlap}, K={info['K']}, "
+                            f"V={info['V']}, E={info['E']}, {args.level}-level DDM-GNN "
+                            f"k_bar={info['k_bar']} d={info['d']}",
+                "step": "one preconditioner apply z = M r",
+                "l2": "flushed (256 MB write) before every timed step",
+                "parallelism": f"{world} rank(s); each rank owns a full config-C instance",
+            },
+            "roofline": {
+                "kernel": "gnn_kernel (fused restriction + 10 message-passing layers + decoder)",
+                "bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp32_peak, "traffic": None,
+                "algorithmic": f"F_gnn = k(2120 V + 160 E) + 220 V = {flops:.3e} flop per launch",
+                "peak_source": "148 SM x 128 FP32 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json); "
+                               "MEASURED_PEAKS has no FP32 CUDA-core figure",
+                "gnn_ms": gnn_ms, "share_of_step": gnn_ms / ms,
+            },
+            "roofline_spmv": {
+                "bound": "hbm", "achieved": spmv_bytes / (spmv_ms * 1e-3) / 1e9, "peak": hbm_peak,
+                "unit": "GB/s", "frac": spmv_bytes / (spmv_ms * 1e-3) / 1e9 / hbm_peak,
+                "traffic": None, "ms": spmv_ms, "algorithmic_bytes": spmv_bytes,
+            },
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
+                    "d2h_bytes_per_step": 8 * n},
+            "gpu_launches": per_step_launches * args.steps,
+            "clocks": clocks,
+            "pcg": pcg,
+            "setup_s": {"problem_build": t_setup, "preconditioner_build": t_build},
+        }
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -20,6 +20,7 @@ LIB_PATH = os.path.join(_HERE, "libddmgnn_b200.so")
 PRECOND_NONE = 0
 LEVEL_ONE = 1
 LEVEL_TWO = 2
+LEGACY_STREAM = 1  # cudaStreamLegacy
 
 _i64 = ctypes.c_int64
 _i32 = ctypes.c_int32

@@ -76,7 +76,9 @@ struct ddmgnn_ctx {
   bool have_model = false;
   PackedModel model;
   float* d_bank = nullptr;
-  int n_big = 0, k_max_big = 0, k_max_small = 0;
+  int n_big = 0;          // subdomains whose node state does not fit shared memory
+  size_t gnn_smem = 0;
+  int cap0 = 0, cap1 = 0;
   // coarse
   int coarse_k = 0;
   double* d_cinv = nullptr;
@@ -288,26 +290,27 @@ static cudaError_t upload(T** dst, const std::vector<T>& v) {
   return cudaMemcpy(*dst, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice);
 }
 
-// Split subdomains into the SMEM class and the global-scratch class for the
-// current latent dimension and (re)allocate the chunk scratch.
+// Plan the shared-memory placement for the current latent dimension and
+// (re)allocate the per-node global scratch it needs.
 static int refresh_classes(ddmgnn_ctx* c) {
   if (!c->built || !c->have_model) return kOk;
-  const int cap = gnn_smem_max_nodes(c->model.d);
-  const auto& ord = c->lay.h_order;
-  const auto& sp = c->lay.h_sub_ptr;
-  int nb = 0;
-  while (nb < c->K && sp[ord[nb] + 1] - sp[ord[nb]] > cap) ++nb;
-  c->n_big = nb;
-  c->k_max_big = nb ? sp[ord[0] + 1] - sp[ord[0]] : 0;
-  c->k_max_small = nb < c->K ? sp[ord[nb] + 1] - sp[ord[nb]] : 0;
   const int d = c->model.d;
+  c->gnn_smem = gnn_plan_smem(d, c->lay.k_max, &c->cap0, &c->cap1);
+  const auto& sp = c->lay.h_sub_ptr;
+  int nb = 0, n2 = 0;
+  for (int i = 0; i < c->K; ++i) {
+    const int k = sp[i + 1] - sp[i];
+    nb += k > c->cap0;
+    n2 += k > c->cap1;
+  }
+  c->n_big = nb;
   const int hs = (d % 2 == 0) ? d : d + 1;
   const int qs = (2 * d + 3) / 4 * 4;
   const size_t V = c->lay.V;
   const bool multi = c->model.n_chunks() > 1;
   CUDA_TRY(dalloc(&c->d_hbuf, (multi || nb) ? V * hs : 0));
   CUDA_TRY(dalloc(&c->d_cbuf, (multi || nb) ? V : 0));
-  CUDA_TRY(dalloc(&c->d_qbuf, nb ? V * qs : 0));
+  CUDA_TRY(dalloc(&c->d_qbuf, n2 ? V * qs : 0));
   return kOk;
 }
 
@@ -435,16 +438,11 @@ static cudaError_t enqueue_gnn(ddmgnn_ctx* c, const double* r, int* status, cons
     a.last = ch == nch - 1;
     a.layer0 = ch * M.lmax + 1;
     a.nl = std::min(M.lmax, M.k_bar - ch * M.lmax);
-    if (c->n_big) {
-      a.order_begin = 0;
-      e = launch_gnn(M.d, false, c->n_big, c->k_max_big, a, s);
-      if (e != cudaSuccess) return e;
-    }
-    if (c->K - c->n_big) {
-      a.order_begin = c->n_big;
-      e = launch_gnn(M.d, true, c->K - c->n_big, c->k_max_small, a, s);
-      if (e != cudaSuccess) return e;
-    }
+    a.order_begin = 0;
+    a.cap0 = c->cap0;
+    a.cap1 = c->cap1;
+    e = launch_gnn(M.d, c->K, c->lay.k_max, c->gnn_smem, a, s);
+    if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
@@ -600,8 +598,10 @@ static int get_graph(ddmgnn_ctx* c, int level, cudaGraphExec_t* out) {
 
 static int ensure_hist(ddmgnn_ctx* c, int max_iter) {
   if (c->hist_cap < max_iter + 1) {
-    CUDA_TRY(dalloc(&c->d_hist, max_iter + 1));
-    c->hist_cap = max_iter + 1;
+    const int cap = std::max(max_iter + 1, 1024);
+    CUDA_TRY(dalloc(&c->d_hist, cap));
+    c->hist_cap = cap;
+    free_graphs(c);  // captured iterations reference the old history buffer
   }
   return kOk;
 }

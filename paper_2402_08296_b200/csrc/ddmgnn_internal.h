@@ -48,6 +48,7 @@ enum DevStatus : int {
 
 constexpr int kGnnThreads = 512;
 constexpr int kConstFloats = 16384;  // 64 KB constant bank
+constexpr int kGnnSmemMax = 227 * 1024 - 1024;  // dynamic smem cap (static smem < 1 KB)
 
 struct DeviceLayout {
   int n = 0, K = 0, V = 0, S = 0, k_max = 0;
@@ -119,13 +120,15 @@ struct GnnArgs {
   int nl;            // layers in this chunk
   int first, last;   // chunk flags
   int order_begin;   // CTA b handles subdomain order[order_begin + b]
+  int cap0, cap1;    // per-CTA node-state placement thresholds (gnn_plan_smem)
 };
 int gnn_smem_max_nodes(int d);
 // WSRC WDST WE B1 W2O B2O W2I B2I WP1 BP1 WP2 BP2 STRIDE D2P DP DEC_W1 DEC_B1 DEC_W2 DEC_B2 LMAX
 int gnn_bank_offsets(int d, int* o);
 cudaError_t gnn_configure_device();
 cudaError_t upload_bank(int d, const float* dev_bank, cudaStream_t s);  // D2D into the constant bank
-cudaError_t launch_gnn(int d, bool smem_variant, int n_ctas, int k_max, const GnnArgs& a,
+size_t gnn_plan_smem(int d, int k_max, int* cap0, int* cap1);
+cudaError_t launch_gnn(int d, int n_ctas, int k_max, size_t smem, const GnnArgs& a,
                        cudaStream_t s);
 
 // krylov.cu

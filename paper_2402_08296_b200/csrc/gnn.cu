@@ -12,8 +12,8 @@ namespace ddmgnn {
 #define X(DD)                                                                    \
   cudaError_t gnn_configure_d##DD();                                             \
   cudaError_t gnn_upload_d##DD(const float* dev_bank, cudaStream_t s);           \
-  cudaError_t gnn_launch_d##DD(bool smem_variant, int n_ctas, int k_max,         \
-                               const GnnArgs& a, cudaStream_t s);
+  cudaError_t gnn_launch_d##DD(int n_ctas, int k_max, size_t smem, const GnnArgs& a, \
+                               cudaStream_t s);
 DDM_GNN_DIMS(X)
 #undef X
 
@@ -59,7 +59,7 @@ int gnn_bank_offsets(int d, int* o) {
 }
 int gnn_smem_max_nodes(int d) {
   const int nb = gnn_smem_node_bytes(d);
-  return nb ? (227 * 1024 - 1024) / nb : 0;
+  return nb ? kGnnSmemMax / nb : 0;
 }
 
 cudaError_t gnn_configure_device() {
@@ -82,11 +82,35 @@ cudaError_t upload_bank(int d, const float* dev_bank, cudaStream_t s) {
   }
 }
 
-cudaError_t launch_gnn(int d, bool smem_variant, int n_ctas, int k_max, const GnnArgs& a,
+// Shared-memory plan for a launch whose largest subdomain has k_max nodes:
+// returns the dynamic smem bytes and the per-CTA mode thresholds cap0/cap1.
+size_t gnn_plan_smem(int d, int k_max, int* cap0, int* cap1) {
+  const int node0 = gnn_smem_node_bytes(d);            // h + Q + c
+  int qs = 0;
+  switch (d) {
+#define X(DD) case DD: qs = Cfg<DD>::QS; break;
+    DDM_GNN_DIMS(X)
+#undef X
+    default: break;
+  }
+  const int node1 = 4 * qs;                            // Q only
+  const size_t m0 = static_cast<size_t>(k_max) * node0;
+  const size_t m1 = static_cast<size_t>(k_max) * node1;
+  size_t smem;
+  if (m0 <= static_cast<size_t>(kGnnSmemMax)) smem = m0;
+  else if (m1 <= static_cast<size_t>(kGnnSmemMax)) smem = kGnnSmemMax;  // mixed modes 0/1
+  else smem = kGnnSmemMax;
+  *cap0 = node0 ? static_cast<int>(smem / node0) : 0;
+  *cap1 = node1 ? static_cast<int>(smem / node1) : 0;
+  // restriction scratch (k doubles) aliases Q: guaranteed since QS >= 2
+  return smem;
+}
+
+cudaError_t launch_gnn(int d, int n_ctas, int k_max, size_t smem, const GnnArgs& a,
                        cudaStream_t s) {
   if (n_ctas <= 0) return cudaSuccess;
   switch (d) {
-#define X(DD) case DD: return gnn_launch_d##DD(smem_variant, n_ctas, k_max, a, s);
+#define X(DD) case DD: return gnn_launch_d##DD(n_ctas, k_max, smem, a, s);
     DDM_GNN_DIMS(X)
 #undef X
     default: return cudaErrorInvalidValue;

@@ -18,19 +18,9 @@ static __constant__ float c_w[kConstFloats];
 
 namespace ddmgnn {
 
-template <bool SV>
-static cudaError_t launch_one(int n_ctas, int k_max, const GnnArgs& a, cudaStream_t s) {
-  const size_t smem = SV ? static_cast<size_t>(k_max) * Cfg<GNN_D>::SMEM_NODE_BYTES : 0;
-  int threads = ((k_max + 31) / 32) * 32;
-  if (threads > kGnnThreads) threads = kGnnThreads;
-  if (threads < 64) threads = 64;
-  gnn_kernel<GNN_D, SV><<<n_ctas, threads, smem, s>>>(a);
-  return cudaGetLastError();
-}
-
 cudaError_t DDM_CAT(gnn_configure_d, GNN_D)() {
-  return cudaFuncSetAttribute(gnn_kernel<GNN_D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              227 * 1024 - 1024);
+  return cudaFuncSetAttribute(gnn_kernel<GNN_D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              kGnnSmemMax);
 }
 
 cudaError_t DDM_CAT(gnn_upload_d, GNN_D)(const float* dev_bank, cudaStream_t s) {
@@ -38,10 +28,15 @@ cudaError_t DDM_CAT(gnn_upload_d, GNN_D)(const float* dev_bank, cudaStream_t s) 
                                  cudaMemcpyDeviceToDevice, s);
 }
 
-cudaError_t DDM_CAT(gnn_launch_d, GNN_D)(bool smem_variant, int n_ctas, int k_max,
-                                         const GnnArgs& a, cudaStream_t s) {
-  return smem_variant ? launch_one<true>(n_ctas, k_max, a, s)
-                      : launch_one<false>(n_ctas, k_max, a, s);
+// One launch over n_ctas subdomains; k_max = largest subdomain, smem = dynamic
+// shared memory chosen by the host (gnn_plan_smem).
+cudaError_t DDM_CAT(gnn_launch_d, GNN_D)(int n_ctas, int k_max, size_t smem, const GnnArgs& a,
+                                         cudaStream_t s) {
+  int threads = ((k_max + 31) / 32) * 32;
+  if (threads > kGnnThreads) threads = kGnnThreads;
+  if (threads < 64) threads = 64;
+  gnn_kernel<GNN_D><<<n_ctas, threads, smem, s>>>(a);
+  return cudaGetLastError();
 }
 
 }  // namespace ddmgnn

@@ -106,18 +106,25 @@ __device__ __forceinline__ void matvec_acc(const float (&x)[NIN], float (&acc)[N
   }
 }
 
-// Per-CTA views of the node state: SMEM (SV) or per-node global scratch.
-template <int D, bool SV>
+// Per-CTA views of the node state.  MODE 0: h, Q, c in shared memory; MODE 1: Q in
+// shared memory, h and c in per-node global scratch; MODE 2: everything in global
+// scratch (L1/L2 resident).  The mode is chosen per CTA from the subdomain size, so
+// one launch covers every subdomain.
+template <int D, int MODE>
 struct NodeState {
   float* h;  // k rows of HS floats
   float* q;  // k rows of QS floats
   float* c;  // k floats
   __device__ __forceinline__ NodeState(int k, float* gq, float* gh, float* gc) {
-    if constexpr (SV) {
-      extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    if constexpr (MODE == 0) {
       q = reinterpret_cast<float*>(smem_raw);
       h = q + static_cast<size_t>(k) * Cfg<D>::QS;
       c = h + static_cast<size_t>(k) * Cfg<D>::HS;
+    } else if constexpr (MODE == 1) {
+      q = reinterpret_cast<float*>(smem_raw);
+      h = gh;
+      c = gc;
     } else {
       q = gq;
       h = gh;
@@ -128,7 +135,7 @@ struct NodeState {
 
 // One message-passing layer for the CTA's subdomain.  L is the layer's slot in
 // the constant bank (compile-time, so every weight address is an immediate).
-template <int D, int L, bool SV>
+template <int D, int L, int MODE>
 __device__ __noinline__ void gnn_layer(int k, float* gq, float* gh, float* gc,
                                        const float4* __restrict__ edges,
                                        const int* __restrict__ slice_off,
@@ -138,7 +145,7 @@ __device__ __noinline__ void gnn_layer(int k, float* gq, float* gh, float* gc,
   constexpr int W = L * C::STRIDE;
   constexpr int D2 = C::D2;
   const int tid = threadIdx.x, nthr = blockDim.x;
-  NodeState<D, SV> ns(k, gq, gh, gc);
+  NodeState<D, MODE> ns(k, gq, gh, gc);
   // ---- phase A: destination projections Q_t = h_t . W1cat[d:2d] ----
   for (int n = tid; n < k; n += nthr) {
     float h[D];
@@ -230,7 +237,7 @@ __device__ __noinline__ void gnn_layer(int k, float* gq, float* gh, float* gc,
   __syncthreads();
 }
 
-template <int D, int L, bool SV>
+template <int D, int L, int MODE>
 struct LayerLoop {
   __device__ __forceinline__ static void run(int nl, int k, float* gq, float* gh, float* gc,
                                              const float4* edges, const int* slice_off,
@@ -238,8 +245,8 @@ struct LayerLoop {
                                              int layer0) {
     if constexpr (L < Cfg<D>::LMAX) {
       if (L < nl) {
-        gnn_layer<D, L, SV>(k, gq, gh, gc, edges, slice_off, deg, alpha, bad, layer0 + L);
-        LayerLoop<D, L + 1, SV>::run(nl, k, gq, gh, gc, edges, slice_off, deg, alpha, bad,
+        gnn_layer<D, L, MODE>(k, gq, gh, gc, edges, slice_off, deg, alpha, bad, layer0 + L);
+        LayerLoop<D, L + 1, MODE>::run(nl, k, gq, gh, gc, edges, slice_off, deg, alpha, bad,
                                      layer0);
       }
     }
@@ -252,25 +259,25 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// SV (SMEM variant): h, Q and c of the subdomain live in shared memory.  Otherwise
-// they live in per-node global scratch (hbuf/qbuf/cbuf, L1/L2 resident) so that
-// arbitrarily large subdomains are supported.
-template <int D, bool SV>
-__global__ void __launch_bounds__(kGnnThreads, 1) gnn_kernel(GnnArgs a) {
-  using C = Cfg<D>;
-  if (a.skip != nullptr && *a.skip != 0) return;
-  __shared__ double red[2][kGnnThreads / 32];
-  __shared__ int sh_bad;
-  __shared__ double sh_scale;
+struct GnnShared {
+  double red[2][kGnnThreads / 32];
+  int bad;
+  double scale;
+};
 
+template <int D, int MODE>
+__device__ __forceinline__ void gnn_body(const GnnArgs& a, GnnShared& sh, int sub, int pos0,
+                                         int k) {
+  using C = Cfg<D>;
+  constexpr bool SV = MODE == 0;  // node state fully in shared memory
   const int tid = threadIdx.x, nthr = blockDim.x;
-  const int sub = a.order[a.order_begin + blockIdx.x];
-  const int pos0 = a.sub_ptr[sub];
-  const int k = a.sub_ptr[sub + 1] - pos0;
-  float* gq = SV ? nullptr : a.qbuf + static_cast<size_t>(pos0) * C::QS;
-  float* gh = SV ? nullptr : a.hbuf + static_cast<size_t>(pos0) * C::HS;
-  float* gc = SV ? nullptr : a.cbuf + pos0;
-  NodeState<D, SV> ns(k, gq, gh, gc);
+  float* gq = MODE == 2 ? a.qbuf + static_cast<size_t>(pos0) * C::QS : nullptr;
+  float* gh = MODE >= 1 ? a.hbuf + static_cast<size_t>(pos0) * C::HS : nullptr;
+  float* gc = MODE >= 1 ? a.cbuf + pos0 : nullptr;
+  NodeState<D, MODE> ns(k, gq, gh, gc);
+  double (&red)[2][kGnnThreads / 32] = sh.red;
+  int& sh_bad = sh.bad;
+  double& sh_scale = sh.scale;
   if (tid == 0) sh_bad = 0;
 
   double s;
@@ -338,7 +345,7 @@ __global__ void __launch_bounds__(kGnnThreads, 1) gnn_kernel(GnnArgs a) {
   }
   __syncthreads();
 
-  LayerLoop<D, 0, SV>::run(a.nl, k, gq, gh, gc, a.edges, a.slice_off + a.slice_base[sub],
+  LayerLoop<D, 0, MODE>::run(a.nl, k, gq, gh, gc, a.edges, a.slice_off + a.slice_base[sub],
                            a.deg + pos0, a.alpha, &sh_bad, a.layer0);
 
   int outbad = 0;
@@ -375,6 +382,25 @@ __global__ void __launch_bounds__(kGnnThreads, 1) gnn_kernel(GnnArgs a) {
       if (outbad) a.out_bad[sub] = 1;
     }
     if (b != 0 || outbad) atomicMax(a.status, static_cast<int>(kPrecondError));
+  }
+}
+
+// One CTA per subdomain (LPT order); the node-state placement is chosen per CTA:
+// a.cap0 = largest k with h, Q, c in the launch's shared memory, a.cap1 = largest
+// k with Q alone in shared memory.
+template <int D>
+__global__ void __launch_bounds__(kGnnThreads, 1) gnn_kernel(GnnArgs a) {
+  if (a.skip != nullptr && *a.skip != 0) return;
+  __shared__ GnnShared sh;
+  const int sub = a.order[a.order_begin + blockIdx.x];
+  const int pos0 = a.sub_ptr[sub];
+  const int k = a.sub_ptr[sub + 1] - pos0;
+  if (k <= a.cap0) {
+    gnn_body<D, 0>(a, sh, sub, pos0, k);
+  } else if (k <= a.cap1) {
+    gnn_body<D, 1>(a, sh, sub, pos0, k);
+  } else {
+    gnn_body<D, 2>(a, sh, sub, pos0, k);
   }
 }
 

@@ -151,7 +151,8 @@ def apply_ddm_gnn(p: DdmGnnPreconditioner, r):
             raise ValueError(f"expected vector of length {n}, got shape {tuple(r.shape)}")
         r = r.to(dtype=torch.float64).contiguous()
         z = torch.empty_like(r)
-        stream = torch.cuda.current_stream(r.device).cuda_stream
+        # torch's default stream is the legacy NULL stream: pass cudaStreamLegacy (0x1)
+        stream = torch.cuda.current_stream(r.device).cuda_stream or _lib.LEGACY_STREAM
         p.context.apply_device(r.data_ptr(), z.data_ptr(), p._level_code, stream, True)
         return z
     r = np.asarray(r, dtype=float)
