@@ -59,6 +59,8 @@ static void dfree(T*& p) {
 struct ddmgnn_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // big-subdomain GNN kernel (forked from the apply stream)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // matrix
   int n = 0;
   long long nnz = 0;
@@ -122,6 +124,13 @@ extern "C" int ddmgnn_create(int device, ddmgnn_ctx** out) {
     delete c;
     return fail(kCudaError, cudaGetErrorString(e));
   }
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(kCudaError, cudaGetErrorString(e));
+  }
   e = cudaMallocHost(reinterpret_cast<void**>(&c->h_st), sizeof(PcgState));
   if (e != cudaSuccess) {
     cudaStreamDestroy(c->stream);
@@ -142,7 +151,7 @@ static void free_graphs(ddmgnn_ctx* c) {
 static void free_layout(ddmgnn_ctx* c) {
   DeviceLayout& L = c->lay;
   dfree(L.sub_ptr); dfree(L.idx); dfree(L.order); dfree(L.slice_base); dfree(L.slice_off);
-  dfree(L.deg); dfree(L.edges); dfree(L.tptr); dfree(L.tent); dfree(L.pou);
+  dfree(L.deg); dfree(L.edges); dfree(L.xy); dfree(L.tptr); dfree(L.tent); dfree(L.pou);
   dfree(c->d_r0r); dfree(c->d_scale); dfree(c->d_zloc); dfree(c->d_y);
   dfree(c->d_bad); dfree(c->d_outbad);
   dfree(c->d_hbuf); dfree(c->d_cbuf); dfree(c->d_qbuf);
@@ -164,6 +173,9 @@ extern "C" void ddmgnn_destroy(ddmgnn_ctx* c) {
   if (c->h_pin_a) cudaFreeHost(c->h_pin_a);
   if (c->h_pin_b) cudaFreeHost(c->h_pin_b);
   cudaStreamDestroy(c->stream);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   delete c;
 }
 
@@ -308,9 +320,9 @@ static int refresh_classes(ddmgnn_ctx* c) {
   const int qs = (2 * d + 3) / 4 * 4;
   const size_t V = c->lay.V;
   const bool multi = c->model.n_chunks() > 1;
-  CUDA_TRY(dalloc(&c->d_hbuf, (multi || nb) ? V * hs : 0));
+  CUDA_TRY(dalloc(&c->d_hbuf, (multi || nb) ? (V + c->K) * hs : 0));  // + dummy row per subdomain
   CUDA_TRY(dalloc(&c->d_cbuf, (multi || nb) ? V : 0));
-  CUDA_TRY(dalloc(&c->d_qbuf, n2 ? V * qs : 0));
+  CUDA_TRY(dalloc(&c->d_qbuf, n2 ? (V + c->K) * qs : 0));  // + one dummy row per subdomain
   return kOk;
 }
 
@@ -346,6 +358,8 @@ extern "C" int ddmgnn_build(ddmgnn_ctx* c) {
   if (H.E_pad)
     CUDA_TRY(cudaMemcpy(L.edges, H.edges.data(), sizeof(float) * H.edges.size(),
                         cudaMemcpyHostToDevice));
+  CUDA_TRY(dalloc(&L.xy, std::max(H.V, 1)));
+  CUDA_TRY(cudaMemcpy(L.xy, H.xy.data(), sizeof(float) * H.xy.size(), cudaMemcpyHostToDevice));
   CUDA_TRY(upload(&L.tptr, H.tptr));
   CUDA_TRY(dalloc(&L.tent, std::max(H.V, 1)));
   CUDA_TRY(cudaMemcpy(L.tent, H.tent.data(), sizeof(int) * H.tent.size(), cudaMemcpyHostToDevice));
@@ -385,21 +399,26 @@ extern "C" int ddmgnn_export_local_graph(ddmgnn_ctx* c, int64_t sub, int64_t* n_
   const int ns = (k + 31) / 32;
   std::vector<int> so(ns + 1);
   CUDA_TRY(cudaMemcpy(so.data(), L.slice_off + sb, sizeof(int) * (ns + 1), cudaMemcpyDeviceToHost));
-  std::vector<float4> rec(std::max(so[ns] - so[0], 1));
+  std::vector<float2> rec(std::max(so[ns] - so[0], 1));
   if (so[ns] > so[0])
-    CUDA_TRY(cudaMemcpy(rec.data(), L.edges + so[0], sizeof(float4) * (so[ns] - so[0]),
+    CUDA_TRY(cudaMemcpy(rec.data(), L.edges + so[0], sizeof(float2) * (so[ns] - so[0]),
                         cudaMemcpyDeviceToHost));
+  std::vector<int> gidx(std::max(k, 1));
+  if (k) CUDA_TRY(cudaMemcpy(gidx.data(), L.idx + b, sizeof(int) * k, cudaMemcpyDeviceToHost));
   int64_t o = 0;
   for (int a = 0; a < k; ++a) {
     for (int e = 0; e < deg[a]; ++e) {
-      const float4 r = rec[so[a >> 5] - so[0] + 32 * e + (a & 31)];
+      const float2 r = rec[so[a >> 5] - so[0] + 32 * e + (a & 31)];
       src[o] = a;
       int t;
-      std::memcpy(&t, &r.w, 4);
+      std::memcpy(&t, &r.y, 4);
       dst[o] = t;
-      vec3[3 * o] = r.x;
-      vec3[3 * o + 1] = r.y;
-      vec3[3 * o + 2] = r.z;
+      // the device folds edge_vec into per-node projections; report the fp32
+      // rounding of the fp64 difference it stands for (dss.py:184)
+      const int gs = gidx[a], gt = gidx[t];
+      vec3[3 * o] = static_cast<float>(c->coords[2 * gt] - c->coords[2 * gs]);
+      vec3[3 * o + 1] = static_cast<float>(c->coords[2 * gt + 1] - c->coords[2 * gs + 1]);
+      vec3[3 * o + 2] = r.x;
       ++o;
     }
   }
@@ -425,7 +444,7 @@ static cudaError_t enqueue_gnn(ddmgnn_ctx* c, const double* r, int* status, cons
   const PackedModel& M = c->model;
   GnnArgs a{};
   a.sub_ptr = L.sub_ptr; a.idx = L.idx; a.order = L.order; a.slice_base = L.slice_base;
-  a.slice_off = L.slice_off; a.deg = L.deg; a.edges = L.edges; a.pou = L.pou;
+  a.slice_off = L.slice_off; a.deg = L.deg; a.edges = L.edges; a.xy = L.xy; a.pou = L.pou;
   a.r = r; a.r0r = c->d_r0r; a.scale = c->d_scale; a.zloc = c->d_zloc;
   a.hbuf = c->d_hbuf; a.cbuf = c->d_cbuf; a.qbuf = c->d_qbuf;
   a.bad_layer = c->d_bad; a.out_bad = c->d_outbad; a.status = status; a.skip = skip;
@@ -441,7 +460,11 @@ static cudaError_t enqueue_gnn(ddmgnn_ctx* c, const double* r, int* status, cons
     a.order_begin = 0;
     a.cap0 = c->cap0;
     a.cap1 = c->cap1;
-    e = launch_gnn(M.d, c->K, c->lay.k_max, c->gnn_smem, a, s);
+    const int k_small = c->n_big < c->K ? c->lay.h_sub_ptr[c->lay.h_order[c->n_big] + 1] -
+                                              c->lay.h_sub_ptr[c->lay.h_order[c->n_big]]
+                                        : 0;
+    e = launch_gnn(M.d, c->K, c->n_big, c->lay.k_max, k_small, c->gnn_smem, a, s, c->side,
+                   c->ev_fork, c->ev_join);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

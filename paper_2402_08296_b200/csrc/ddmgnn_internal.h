@@ -9,10 +9,13 @@
 //   Local graphs in SELL-32 ("sliced ELL", slice = 32 consecutive local nodes =
 //   one warp): slice q of subdomain i holds w_q = max degree in the slice; record
 //   (e, lane) of the slice lives at edges[slice_off[slice_base[i]+q] + 32*e + lane].
-//   A record is float4 {dx, dy, |d|, bits(dst_local)}: the reference's edge_vec /
-//   edge_len (dss.py:184-185, computed in fp64 then rounded to fp32) and the local
-//   destination.  Records of one node are in ascending dst order, i.e. the
-//   reference's lexsorted (src, dst) edge order (dss.py:181).
+//   A record is float2 {|d|, bits(dst_local)}: the reference's edge_len
+//   (dss.py:185, computed in fp64 then rounded to fp32) and the local destination.
+//   Records of one node are in ascending dst order, i.e. the reference's
+//   lexsorted (src, dst) edge order (dss.py:181).  The relative position
+//   edge_vec = coords[dst] - coords[src] (dss.py:184) is folded into the per-node
+//   projections, so per node the kernel reads
+//   xy[V]         float2 fp32(coords - centre of the node's subdomain)
 //   deg[V]        uint16 out-degree of every batched node
 //   tptr[N+1], tent[V] (int2: batched position, subdomain) — transpose map used
 //                 by the gather-based prolongation, ascending subdomain per DOF
@@ -56,7 +59,8 @@ struct DeviceLayout {
   int *sub_ptr = nullptr, *idx = nullptr, *order = nullptr;
   int *slice_base = nullptr, *slice_off = nullptr;
   uint16_t* deg = nullptr;
-  float4* edges = nullptr;
+  float2* edges = nullptr;
+  float2* xy = nullptr;
   int* tptr = nullptr;
   int2* tent = nullptr;
   double* pou = nullptr;
@@ -69,7 +73,8 @@ struct HostLayout {
   long long E = 0, E_pad = 0;
   std::vector<int> sub_ptr, idx, order, slice_base, slice_off;
   std::vector<uint16_t> deg;
-  std::vector<float> edges;  // 4 floats per record
+  std::vector<float> edges;  // 2 floats per record
+  std::vector<float> xy;     // 2 floats per batched node
   std::vector<int> tptr;
   std::vector<int> tent;  // 2 ints per entry
   std::vector<double> pou;
@@ -102,7 +107,8 @@ struct GnnArgs {
   const int* slice_base;
   const int* slice_off;
   const uint16_t* deg;
-  const float4* edges;
+  const float2* edges;
+  const float2* xy;
   const double* pou;
   const double* r;
   double* r0r;
@@ -123,13 +129,14 @@ struct GnnArgs {
   int cap0, cap1;    // per-CTA node-state placement thresholds (gnn_plan_smem)
 };
 int gnn_smem_max_nodes(int d);
-// WSRC WDST WE B1 W2O B2O W2I B2I WP1 BP1 WP2 BP2 STRIDE D2P DP DEC_W1 DEC_B1 DEC_W2 DEC_B2 LMAX
+// WQ WP B1 WL WU BP1 WP2 BP2 STRIDE D2P DP DEC_W1 DEC_B1 DEC_W2 DEC_B2 LMAX (gnn_cfg.h)
 int gnn_bank_offsets(int d, int* o);
 cudaError_t gnn_configure_device();
 cudaError_t upload_bank(int d, const float* dev_bank, cudaStream_t s);  // D2D into the constant bank
 size_t gnn_plan_smem(int d, int k_max, int* cap0, int* cap1);
-cudaError_t launch_gnn(int d, int n_ctas, int k_max, size_t smem, const GnnArgs& a,
-                       cudaStream_t s);
+cudaError_t launch_gnn(int d, int n_ctas, int n_big, int k_max, int k_max_small, size_t smem,
+                       const GnnArgs& a, cudaStream_t s, cudaStream_t side, cudaEvent_t fork,
+                       cudaEvent_t join);
 
 // krylov.cu
 struct PcgState {

@@ -9,11 +9,15 @@
 
 namespace ddmgnn {
 
-#define X(DD)                                                                    \
-  cudaError_t gnn_configure_d##DD();                                             \
-  cudaError_t gnn_upload_d##DD(const float* dev_bank, cudaStream_t s);           \
-  cudaError_t gnn_launch_d##DD(int n_ctas, int k_max, size_t smem, const GnnArgs& a, \
-                               cudaStream_t s);
+#define X(DD)                                                                        \
+  cudaError_t gnn_configure_d##DD();                                                 \
+  cudaError_t gnn_upload_d##DD(const float* dev_bank, cudaStream_t s);               \
+  cudaError_t gnn_launch_d##DD(int n_ctas, int k_max, size_t smem, const GnnArgs& a,  \
+                               cudaStream_t s);                                      \
+  cudaError_t gnn_configure_big_d##DD();                                             \
+  cudaError_t gnn_upload_big_d##DD(const float* dev_bank, cudaStream_t s);           \
+  cudaError_t gnn_launch_big_d##DD(int n_ctas, int k_max, size_t smem, const GnnArgs& a, \
+                                   cudaStream_t s);
 DDM_GNN_DIMS(X)
 #undef X
 
@@ -67,6 +71,8 @@ cudaError_t gnn_configure_device() {
   {                                             \
     cudaError_t e = gnn_configure_d##DD();      \
     if (e != cudaSuccess) return e;             \
+    e = gnn_configure_big_d##DD();              \
+    if (e != cudaSuccess) return e;             \
   }
   DDM_GNN_DIMS(X)
 #undef X
@@ -75,7 +81,11 @@ cudaError_t gnn_configure_device() {
 
 cudaError_t upload_bank(int d, const float* dev_bank, cudaStream_t s) {
   switch (d) {
-#define X(DD) case DD: return gnn_upload_d##DD(dev_bank, s);
+#define X(DD)                                                  \
+  case DD: {                                                   \
+    cudaError_t e = gnn_upload_d##DD(dev_bank, s);             \
+    return e != cudaSuccess ? e : gnn_upload_big_d##DD(dev_bank, s); \
+  }
     DDM_GNN_DIMS(X)
 #undef X
     default: return cudaErrorInvalidValue;
@@ -94,27 +104,54 @@ size_t gnn_plan_smem(int d, int k_max, int* cap0, int* cap1) {
     default: break;
   }
   const int node1 = 4 * qs;                            // Q only
-  const size_t m0 = static_cast<size_t>(k_max) * node0;
-  const size_t m1 = static_cast<size_t>(k_max) * node1;
+  // +1 node: the dummy Q row addressed by SELL padding records
+  const size_t m0 = static_cast<size_t>(k_max + 1) * node0;
+  const size_t m1 = static_cast<size_t>(k_max + 1) * node1;
   size_t smem;
   if (m0 <= static_cast<size_t>(kGnnSmemMax)) smem = m0;
   else if (m1 <= static_cast<size_t>(kGnnSmemMax)) smem = kGnnSmemMax;  // mixed modes 0/1
   else smem = kGnnSmemMax;
-  *cap0 = node0 ? static_cast<int>(smem / node0) : 0;
-  *cap1 = node1 ? static_cast<int>(smem / node1) : 0;
+  *cap0 = node0 ? static_cast<int>(smem / node0) - 1 : 0;
+  *cap1 = node1 ? static_cast<int>(smem / node1) - 1 : 0;
   // restriction scratch (k doubles) aliases Q: guaranteed since QS >= 2
   return smem;
 }
 
-cudaError_t launch_gnn(int d, int n_ctas, int k_max, size_t smem, const GnnArgs& a,
-                       cudaStream_t s) {
+// Launch the GNN over all subdomains of `order` (LPT, descending size): the first
+// n_big (k > cap0) run in gnn_big_kernel on the side stream `side`, concurrently
+// with gnn_kernel over the rest on `s` (fork/join by events, graph-capturable).
+cudaError_t launch_gnn(int d, int n_ctas, int n_big, int k_max, int k_max_small, size_t smem,
+                       const GnnArgs& a, cudaStream_t s, cudaStream_t side, cudaEvent_t fork,
+                       cudaEvent_t join) {
   if (n_ctas <= 0) return cudaSuccess;
-  switch (d) {
-#define X(DD) case DD: return gnn_launch_d##DD(n_ctas, k_max, smem, a, s);
-    DDM_GNN_DIMS(X)
+  cudaError_t e;
+  if (n_big > 0) {
+    if ((e = cudaEventRecord(fork, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(side, fork, 0)) != cudaSuccess) return e;
+    GnnArgs b = a;
+    b.order_begin = a.order_begin;
+    switch (d) {
+#define X(DD) case DD: e = gnn_launch_big_d##DD(n_big, k_max, smem, b, side); break;
+      DDM_GNN_DIMS(X)
 #undef X
-    default: return cudaErrorInvalidValue;
+      default: return cudaErrorInvalidValue;
+    }
+    if (e != cudaSuccess) return e;
+    if ((e = cudaEventRecord(join, side)) != cudaSuccess) return e;
   }
+  if (n_ctas > n_big) {
+    GnnArgs m = a;
+    m.order_begin = a.order_begin + n_big;
+    switch (d) {
+#define X(DD) case DD: e = gnn_launch_d##DD(n_ctas - n_big, k_max_small, smem, m, s); break;
+      DDM_GNN_DIMS(X)
+#undef X
+      default: return cudaErrorInvalidValue;
+    }
+    if (e != cudaSuccess) return e;
+  }
+  if (n_big > 0) return cudaStreamWaitEvent(s, join, 0);
+  return cudaSuccess;
 }
 
 }  // namespace ddmgnn

@@ -1,8 +1,18 @@
 // Compile-time layout of the per-layer weight bank and SMEM rows (see gnn_impl.cuh).
 //
 // Every weight matrix is stored row-major [in][out] with rows padded to a multiple
-// of 4 floats, so the innermost (output) loop of every mat-vec reads 16-byte
-// aligned consecutive constants (one LDCU.128 per 4 FFMAs on sm_100).
+// of 4 floats, so the output loop of every mat-vec reads 16-byte aligned
+// consecutive constants: one LDCU.128 feeds two packed FFMA2 (f32x2) on sm_100.
+//
+// The bank holds the reference's weights (dss.py:54-81) after three exact-in-
+// exact-arithmetic rewrites (gnn_impl.cuh explains each):
+//   * edge MLP hidden layer split into per-node projections, with the relative
+//     position dx,dy (= x_t - x_s) folded into them: WQ = [Wdst; +We_xy],
+//     WP = [Wsrc; -We_xy], only the |d| row WL stays per edge;
+//   * the messages' linear second layer (W2, b2) folded through the sum into psi's
+//     first layer: Mo = 0.5 * W2o . Wp1[phi_o rows], Mi likewise, bdeg = b2o .
+//     Wp1[phi_o rows] + b2i . Wp1[phi_i rows] (multiplies the node degree);
+//   * relu(x) = 0.5 (x + |x|): the 0.5 lives in Mo, Mi and WP2.
 #pragma once
 #include "ddmgnn_internal.h"
 
@@ -13,23 +23,22 @@ constexpr int round4(int x) { return (x + 3) / 4 * 4; }
 template <int D>
 struct Cfg {
   static constexpr int D2 = 2 * D;
-  static constexpr int DP = round4(D);       // padded row of a D-wide output
-  static constexpr int D2P = round4(2 * D);  // padded row of a 2D-wide output
-  static constexpr int HS = (D % 2 == 0) ? D : D + 1;  // h row stride in SMEM (floats)
-  static constexpr int QS = D2P;                       // Q row stride in SMEM (float4 rows)
+  static constexpr int DH = (D + 1) / 2 * 2;      // latent width rounded to pairs
+  static constexpr int NPH = DH / 2;               // pairs of a D-wide output
+  static constexpr int NP2 = D;                    // pairs of a 2D-wide output
+  static constexpr int DP = round4(DH);            // padded row of a D-wide output
+  static constexpr int D2P = round4(2 * D);        // padded row of a 2D-wide output
+  static constexpr int HS = DH;                    // h row stride in SMEM (floats)
+  static constexpr int QS = D2P;                   // Q row stride in SMEM (float4 rows)
   // per-layer bank
-  static constexpr int OFF_WSRC = 0;                        // [D][D2P]  W1cat rows 0..D-1
-  static constexpr int OFF_WDST = OFF_WSRC + D * D2P;       // [D][D2P]  W1cat rows D..2D-1
-  static constexpr int OFF_WE = OFF_WDST + D * D2P;         // [3][D2P]  W1cat rows 2D..2D+2
-  static constexpr int OFF_B1 = OFF_WE + 3 * D2P;           // [D2P]     b1cat
-  static constexpr int OFF_W2O = OFF_B1 + D2P;              // [D][DP]
-  static constexpr int OFF_B2O = OFF_W2O + D * DP;          // [DP]
-  static constexpr int OFF_W2I = OFF_B2O + DP;              // [D][DP]
-  static constexpr int OFF_B2I = OFF_W2I + D * DP;          // [DP]
-  static constexpr int OFF_WP1 = OFF_B2I + DP;              // [3D+1][DP]
-  static constexpr int OFF_BP1 = OFF_WP1 + (3 * D + 1) * DP;  // [DP]
-  static constexpr int OFF_WP2 = OFF_BP1 + DP;              // [D][DP]
-  static constexpr int OFF_BP2 = OFF_WP2 + D * DP;          // [DP]
+  static constexpr int OFF_WQ = 0;                            // [D+2][D2P] Wdst ; +We_x ; +We_y
+  static constexpr int OFF_WP = OFF_WQ + (D + 2) * D2P;       // [D+2][D2P] Wsrc ; -We_x ; -We_y
+  static constexpr int OFF_B1 = OFF_WP + (D + 2) * D2P;       // [D2P]      b1cat
+  static constexpr int OFF_WL = OFF_B1 + D2P;                 // [D2P]      |d| row of W1cat
+  static constexpr int OFF_WU = OFF_WL + D2P;                 // [3D+2][DP] Wp1_h; wp1_c; bdeg; Mo; Mi
+  static constexpr int OFF_BP1 = OFF_WU + (3 * D + 2) * DP;   // [DP]
+  static constexpr int OFF_WP2 = OFF_BP1 + DP;                // [D][DP]    0.5 * Wp2
+  static constexpr int OFF_BP2 = OFF_WP2 + D * DP;            // [DP]
   static constexpr int STRIDE = OFF_BP2 + DP;
   // final-layer decoder at the end of every bank: Wd1 [D][DP], bd1 [DP], wd2 [DP], bd2 [4]
   static constexpr int DEC = D * DP + DP + DP + 4;
@@ -39,21 +48,22 @@ struct Cfg {
   static constexpr int DEC_W2 = DEC_B1 + DP;
   static constexpr int DEC_B2 = DEC_W2 + DP;
   static constexpr int LMAX_RAW = (kConstFloats - DEC) / STRIDE;
-  static constexpr int LMAX = LMAX_RAW > 16 ? 16 : LMAX_RAW;
+  static constexpr int LMAX = LMAX_RAW > 10 ? 10 : LMAX_RAW;  // compile-time slots (gnn_impl.cuh)
   static constexpr int SMEM_NODE_BYTES = (HS + QS + 1) * 4;
   static_assert(STRIDE % 4 == 0 && DEC_OFF % 4 == 0, "bank rows must stay 16-byte aligned");
 };
 
 // Offsets for the host-side packer, in this order:
-// WSRC WDST WE B1 W2O B2O W2I B2I WP1 BP1 WP2 BP2 STRIDE D2P DP DEC_W1 DEC_B1 DEC_W2 DEC_B2 LMAX
+// WQ WP B1 WL WU BP1 WP2 BP2 STRIDE D2P DP DEC_W1 DEC_B1 DEC_W2 DEC_B2 LMAX
+constexpr int kBankOffsets = 16;
 template <int D>
 inline void cfg_offsets(int* o) {
   using C = Cfg<D>;
-  const int v[20] = {C::OFF_WSRC, C::OFF_WDST, C::OFF_WE,  C::OFF_B1,   C::OFF_W2O,
-                     C::OFF_B2O,  C::OFF_W2I,  C::OFF_B2I, C::OFF_WP1,  C::OFF_BP1,
-                     C::OFF_WP2,  C::OFF_BP2,  C::STRIDE,  C::D2P,      C::DP,
-                     C::DEC_W1,   C::DEC_B1,   C::DEC_W2,  C::DEC_B2,   C::LMAX};
-  for (int i = 0; i < 20; ++i) o[i] = v[i];
+  const int v[kBankOffsets] = {C::OFF_WQ,  C::OFF_WP,  C::OFF_B1,  C::OFF_WL,
+                               C::OFF_WU,  C::OFF_BP1, C::OFF_WP2, C::OFF_BP2,
+                               C::STRIDE,  C::D2P,     C::DP,      C::DEC_W1,
+                               C::DEC_B1,  C::DEC_W2,  C::DEC_B2,  C::LMAX};
+  for (int i = 0; i < kBankOffsets; ++i) o[i] = v[i];
 }
 
 }  // namespace ddmgnn

@@ -1,6 +1,6 @@
-// One latent dimension of the fused GNN kernel per translation unit (compiled
-// with -DGNN_D=<d>): each unit owns its own 64 KB constant bank, and the units
-// compile in parallel.
+// One latent dimension of the fused GNN kernels per translation unit (compiled
+// with -DGNN_D=<d>; -DGNN_BIG selects the oversized-subdomain kernel): each unit
+// owns its own 64 KB constant bank, and the units compile in parallel.
 #include "ddmgnn_internal.h"
 
 #ifndef GNN_D
@@ -15,27 +15,34 @@ static __constant__ float c_w[kConstFloats];
 
 #define DDM_CAT2(a, b) a##b
 #define DDM_CAT(a, b) DDM_CAT2(a, b)
+#ifdef GNN_BIG
+#define DDM_KERNEL gnn_big_kernel
+#define DDM_NAME(x) DDM_CAT(DDM_CAT(x, _big_d), GNN_D)
+#else
+#define DDM_KERNEL gnn_kernel
+#define DDM_NAME(x) DDM_CAT(DDM_CAT(x, _d), GNN_D)
+#endif
 
 namespace ddmgnn {
 
-cudaError_t DDM_CAT(gnn_configure_d, GNN_D)() {
-  return cudaFuncSetAttribute(gnn_kernel<GNN_D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+cudaError_t DDM_NAME(gnn_configure)() {
+  return cudaFuncSetAttribute(DDM_KERNEL<GNN_D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               kGnnSmemMax);
 }
 
-cudaError_t DDM_CAT(gnn_upload_d, GNN_D)(const float* dev_bank, cudaStream_t s) {
+cudaError_t DDM_NAME(gnn_upload)(const float* dev_bank, cudaStream_t s) {
   return cudaMemcpyToSymbolAsync(c_w, dev_bank, sizeof(float) * kConstFloats, 0,
                                  cudaMemcpyDeviceToDevice, s);
 }
 
-// One launch over n_ctas subdomains; k_max = largest subdomain, smem = dynamic
-// shared memory chosen by the host (gnn_plan_smem).
-cudaError_t DDM_CAT(gnn_launch_d, GNN_D)(int n_ctas, int k_max, size_t smem, const GnnArgs& a,
-                                         cudaStream_t s) {
+// One launch over n_ctas subdomains (order[a.order_begin ...]); k_max = largest
+// subdomain of the launch, smem = dynamic shared memory chosen by the host.
+cudaError_t DDM_NAME(gnn_launch)(int n_ctas, int k_max, size_t smem, const GnnArgs& a,
+                                 cudaStream_t s) {
   int threads = ((k_max + 31) / 32) * 32;
   if (threads > kGnnThreads) threads = kGnnThreads;
   if (threads < 64) threads = 64;
-  gnn_kernel<GNN_D><<<n_ctas, threads, smem, s>>>(a);
+  DDM_KERNEL<GNN_D><<<n_ctas, threads, smem, s>>>(a);
   return cudaGetLastError();
 }
 

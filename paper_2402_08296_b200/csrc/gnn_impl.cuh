@@ -7,24 +7,27 @@
 // One CTA owns one subdomain for the whole chunk of message-passing layers:
 //   prologue  r_i = r[idx_i] (fp64), s_i = ||r_i||_2, c_i = fp32(r_i / s_i),
 //             (R0 r)_i = sum_j pou_j r_j, h = 0            (first chunk only)
-//   layer l   phase A: Q_t = h_t . W1cat[d:2d]               -> SMEM (2d fp32/node)
+//   layer l   phase A (thread per node t):  Q_t = [h_t, x_t, y_t] . WQ   -> SMEM
 //             phase B (thread per node s, out-edges in ascending dst order):
-//                P_s  = h_s . W1cat[0:d] + b1cat
-//                S_s  = sum_e relu(P_s + Q_dst(e) + [dx,dy,|d|]_e . W1cat[2d:2d+3])
-//                phi  = S_s . blockdiag(W2_out, W2_in) + deg_s * [b2_out, b2_in]
-//                h_s += alpha * psi([h_s, c_s, phi_out, phi_in])
+//                P_s  = b1 + [h_s, x_s, y_s] . WP
+//                S2_s = sum_e 2 relu(P_s + Q_dst(e) + |d|_e WL)
+//                u    = 2 relu(bp1 + deg_s bdeg + [h_s, c_s] . Wp1[h,c] + S2_s . M)
+//                h_s += alpha (bp2 + u . (Wp2 / 2))
 //   epilogue  zloc = s_i * fp64(decoder(h))                  (last chunk only)
-// This is the reference's math with the edge MLP factorised: relu(x_e W1 + b1)
-// with x_e = [h_src, h_dst, dx, dy, |d|] splits into per-node products P, Q plus a
-// 3-term edge part, and the second (linear) MLP layer commutes with the scatter-
-// sum (dss.py:319-322), so the per-edge work is 2d*(1 add + 3 FMA + relu + add).
 //
-// All MLP weights of a chunk live in a 64 KB __constant__ bank at compile-time
-// offsets (the layer loop is unrolled over bank slots), so weights reach the FFMAs
-// as uniform-register operands loaded by LDCU.128 — no per-thread loads and no
-// vector register-file pressure.  Arithmetic is FP32 CUDA-core FMA: TF32 tensor
-// cores miss the 1e-5 parity bar (SURVEY.md finding 6).  ReLU propagates NaN like
-// numpy.maximum (max.NaN).
+// This is the reference's arithmetic rewritten without changing its value in
+// exact arithmetic (fp32 rounding differs by O(1e-7); SURVEY.md §8a / DESIGN.md §4):
+//  * edge MLP factorised: relu(x_e W1 + b1) with x_e = [h_src, h_dst, dx, dy, |d|]
+//    and (dx, dy) = xy_dst - xy_src (dss.py:184, subdomain-centred coordinates),
+//    so per edge only P_s + Q_t + |d| WL remains (dss.py:316-318);
+//  * the messages' second (linear) layer commutes with the scatter-sum
+//    (dss.py:319-322) and is folded into psi's first layer (M = W2 . Wp1[phi rows],
+//    bdeg = b2 . Wp1[phi rows] per unit degree);
+//  * relu(x) = (x + |x|) / 2 — one packed FADD2 with an |.| operand instead of two
+//    FMNMX; the 1/2 is folded into M and Wp2.  NaN propagates like numpy.maximum.
+// All per-pair arithmetic is packed f32x2 (FFMA2/FADD2: two FP32 lanes per issue
+// slot), with the weight pair as a uniform-register operand loaded by LDCU.128
+// from a 64 KB __constant__ bank (layer slot = uniform base register + immediate).
 #pragma once
 #include <climits>
 
@@ -41,6 +44,17 @@ __device__ __forceinline__ float relu_nan(float x) {
   float y;
   asm("max.NaN.f32 %0, %1, 0f00000000;" : "=f"(y) : "f"(x));
   return y;
+}
+
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 bcast(float x) { return make_float2(x, x); }
+// 2 relu(x) elementwise: x + |x| (exact; NaN stays NaN)
+__device__ __forceinline__ float2 relu2x(float2 x) {
+  return fadd2(x, make_float2(fabsf(x.x), fabsf(x.y)));
+}
+__device__ __forceinline__ float2 cpair(int off) {
+  return *reinterpret_cast<const float2*>(&c_w[off]);
 }
 
 template <int N>
@@ -78,32 +92,29 @@ __device__ __forceinline__ void store_vec(float* __restrict__ p, const float (&v
   }
 }
 
-template <int D>
-__device__ __forceinline__ void load_h(const float* p, float (&h)[D]) {
-  constexpr int HS = Cfg<D>::HS;
-  float t[HS];
-  load_vec<HS>(p, t);
-#pragma unroll
-  for (int i = 0; i < D; ++i) h[i] = t[i];
-}
-template <int D>
-__device__ __forceinline__ void store_h(float* p, const float (&h)[D]) {
-  constexpr int HS = Cfg<D>::HS;
-  float t[HS];
-#pragma unroll
-  for (int i = 0; i < HS; ++i) t[i] = i < D ? h[i] : 0.f;
-  store_vec<HS>(p, t);
-}
-
-// acc[j] += sum_m x[m] * W[m][j], W at bank offset OFF with row stride RS (outer
-// loop over inputs so every inner step reads consecutive constants).
-template <int NIN, int NOUT, int OFF, int RS>
-__device__ __forceinline__ void matvec_acc(const float (&x)[NIN], float (&acc)[NOUT]) {
+// acc[j] += sum_m x[m] * W[m][2j:2j+2], W at bank offset base + OFF with row stride
+// RS.  `base` is warp-uniform (the layer's slot), so every weight pair is one
+// uniform-register-addressed constant load feeding a packed FFMA2.
+template <int NIN, int NPO, int OFF, int RS>
+__device__ __forceinline__ void mv2(int base, const float (&x)[NIN], float2 (&acc)[NPO]) {
 #pragma unroll
   for (int m = 0; m < NIN; ++m) {
 #pragma unroll
-    for (int j = 0; j < NOUT; ++j) acc[j] = fmaf(x[m], c_w[OFF + m * RS + j], acc[j]);
+    for (int j = 0; j < NPO; ++j)
+      acc[j] = ffma2(bcast(x[m]), cpair(base + OFF + m * RS + 2 * j), acc[j]);
   }
+}
+
+// [h (D), x, y] of a node: h from the node state, (x, y) subdomain-centred coordinates.
+template <int D>
+__device__ __forceinline__ void load_hxy(const float* hrow, float2 xy, float (&v)[D + 2]) {
+  constexpr int DH = Cfg<D>::DH;
+  float t[DH];
+  load_vec<DH>(hrow, t);
+#pragma unroll
+  for (int i = 0; i < D; ++i) v[i] = t[i];
+  v[D] = xy.x;
+  v[D + 1] = xy.y;
 }
 
 // Per-CTA views of the node state.  MODE 0: h, Q, c in shared memory; MODE 1: Q in
@@ -119,8 +130,8 @@ struct NodeState {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if constexpr (MODE == 0) {
       q = reinterpret_cast<float*>(smem_raw);
-      h = q + static_cast<size_t>(k) * Cfg<D>::QS;
-      c = h + static_cast<size_t>(k) * Cfg<D>::HS;
+      h = q + static_cast<size_t>(k + 1) * Cfg<D>::QS;  // Q rows 0..k (k = dummy)
+      c = h + static_cast<size_t>(k + 1) * Cfg<D>::HS;  // h rows 0..k (k = dummy)
     } else if constexpr (MODE == 1) {
       q = reinterpret_cast<float*>(smem_raw);
       h = gh;
@@ -133,125 +144,134 @@ struct NodeState {
   }
 };
 
-// One message-passing layer for the CTA's subdomain.  L is the layer's slot in
-// the constant bank (compile-time, so every weight address is an immediate).
-template <int D, int L, int MODE>
-__device__ __noinline__ void gnn_layer(int k, float* gq, float* gh, float* gc,
-                                       const float4* __restrict__ edges,
-                                       const int* __restrict__ slice_off,
-                                       const uint16_t* __restrict__ deg, float alpha, int* bad,
-                                       int layer_no) {
+// Warp-uniform value (lane 0's): lets ptxas keep loop bounds and the layer's bank
+// offset in uniform registers, so weight pairs are LDCU.128 c[bank][UR + imm]
+// operands of FFMA2 even inside the node loops.
+__device__ __forceinline__ int uni(int v) { return __shfl_sync(0xffffffffu, v, 0); }
+
+// One message-passing layer for the CTA's subdomain.  WT >= 0: the layer's slot
+// offset in the constant bank as a compile-time constant (every weight pair is an
+// immediate-addressed LDCU.128 feeding FFMA2 — the fast path); WT < 0: runtime
+// offset w_rt (used only by the rare big-subdomain kernel).  Node loops run a uniform trip count: warp w of the
+// CTA handles local nodes n0 + lane, n0 = it * nthr + 32 w, i.e. exactly SELL slice
+// n0 / 32, whose width (max degree in the slice) bounds the edge loop.  Padding
+// records point at the dummy Q row k (all -1e30), whose 2 relu term is exactly 0.
+template <int D, int MODE, int WT>
+__device__ __forceinline__ void gnn_layer(int w_rt, int k, int warp, float* gq, float* gh,
+                                          float* gc, const float2* __restrict__ xy,
+                                          const float2* __restrict__ edges,
+                                          const int* __restrict__ slice_off,
+                                          const uint16_t* __restrict__ deg, float alpha,
+                                          int* bad, int layer_no) {
   using C = Cfg<D>;
-  constexpr int W = L * C::STRIDE;
-  constexpr int D2 = C::D2;
-  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int W = WT >= 0 ? WT : w_rt;
+  constexpr int NP2 = C::NP2, NPH = C::NPH;
+  const int lane = threadIdx.x & 31, nthr = blockDim.x;
   NodeState<D, MODE> ns(k, gq, gh, gc);
-  // ---- phase A: destination projections Q_t = h_t . W1cat[d:2d] ----
-  for (int n = tid; n < k; n += nthr) {
-    float h[D];
-    load_h<D>(ns.h + n * C::HS, h);
-    float q[C::QS];
+  // ---- phase A: destination projections Q_t = [h_t, x_t, y_t] . WQ ----
+  for (int n0 = 32 * warp; n0 < k; n0 += nthr) {
+    const int n = n0 + lane;
+    const int nn = min(n, k - 1);
+    float hin[D + 2];
+    load_hxy<D>(ns.h + nn * C::HS, __ldg(xy + nn), hin);
+    float2 q[NP2];
 #pragma unroll
-    for (int j = 0; j < C::QS; ++j) q[j] = 0.f;
-    float qq[D2];
+    for (int j = 0; j < NP2; ++j) q[j] = make_float2(0.f, 0.f);
+    mv2<D + 2, NP2, C::OFF_WQ, C::D2P>(W, hin, q);
+    float qs[C::QS];
 #pragma unroll
-    for (int j = 0; j < D2; ++j) qq[j] = 0.f;
-    matvec_acc<D, D2, W + C::OFF_WDST, C::D2P>(h, qq);
+    for (int j = 0; j < C::QS; ++j) qs[j] = 0.f;
 #pragma unroll
-    for (int j = 0; j < D2; ++j) q[j] = qq[j];
-    store_vec<C::QS>(ns.q + n * C::QS, q);
+    for (int j = 0; j < NP2; ++j) {
+      qs[2 * j] = q[j].x;
+      qs[2 * j + 1] = q[j].y;
+    }
+    // lanes past k recompute node k-1 and store the identical row: no divergent
+    // branch in the loop, so the weight loads stay uniform (LDCU)
+    store_vec<C::QS>(ns.q + nn * C::QS, qs);
   }
   __syncthreads();
-  // ---- phase B: edge aggregation + node update, thread per node ----
+  // ---- phase B: edge aggregation + node update ----
   int first_bad = 0;
-  for (int n = tid; n < k; n += nthr) {
-    float h[D];
-    load_h<D>(ns.h + n * C::HS, h);
-    const float cn = ns.c[n];
-    float p[D2], s[D2];
+  for (int n0 = 32 * warp; n0 < k; n0 += nthr) {
+    const int n = n0 + lane;
+    const int nn = min(n, k - 1);
+    float hin[D + 2];
+    load_hxy<D>(ns.h + nn * C::HS, __ldg(xy + nn), hin);
+    const float cn = ns.c[nn];
+    float2 p[NP2], s[NP2];
 #pragma unroll
-    for (int j = 0; j < D2; ++j) {
-      p[j] = c_w[W + C::OFF_B1 + j];
-      s[j] = 0.f;
+    for (int j = 0; j < NP2; ++j) {
+      p[j] = cpair(W + C::OFF_B1 + 2 * j);
+      s[j] = make_float2(0.f, 0.f);
     }
-    matvec_acc<D, D2, W + C::OFF_WSRC, C::D2P>(h, p);
-    const int dg = deg[n];
-    const float4* ep = edges + slice_off[n >> 5] + (n & 31);
-    float4 rec = dg > 0 ? __ldg(ep) : make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int e = 0; e < dg; ++e) {
-      const float4 cur = rec;
-      if (e + 1 < dg) rec = __ldg(ep + 32 * (e + 1));
-      const int t = __float_as_int(cur.w);
+    mv2<D + 2, NP2, C::OFF_WP, C::D2P>(W, hin, p);
+    const int so = uni(slice_off[n0 >> 5]);
+    const int width = (uni(slice_off[(n0 >> 5) + 1]) - so) >> 5;
+    const float2* ep = edges + so + lane;
+    float2 rec = width > 0 ? __ldg(ep) : make_float2(0.f, 0.f);
+    for (int e = 0; e < width; ++e) {
+      const float2 cur = rec;
+      if (e + 1 < width) rec = __ldg(ep + 32 * (e + 1));
+      const int t = __float_as_int(cur.y);
       float qt[C::QS];
       load_vec<C::QS>(ns.q + t * C::QS, qt);
+      const float2 len = bcast(cur.x);
 #pragma unroll
-      for (int j = 0; j < D2; ++j) {
-        float x = p[j] + qt[j];
-        x = fmaf(cur.x, c_w[W + C::OFF_WE + j], x);
-        x = fmaf(cur.y, c_w[W + C::OFF_WE + C::D2P + j], x);
-        x = fmaf(cur.z, c_w[W + C::OFF_WE + 2 * C::D2P + j], x);
-        s[j] += relu_nan(x);
+      for (int j = 0; j < NP2; ++j) {
+        float2 x = fadd2(p[j], make_float2(qt[2 * j], qt[2 * j + 1]));
+        x = ffma2(len, cpair(W + C::OFF_WL + 2 * j), x);
+        s[j] = fadd2(s[j], relu2x(x));
       }
     }
-    // phi_out / phi_in = S . W2 + deg * b2 (linear second layer commuted with the sum)
-    const float fdeg = static_cast<float>(dg);
-    float x[3 * D + 1];
-    float so[D], si[D], ao[D], ai[D];
+    // psi first layer with the messages' second layer folded in
+    float2 u[NPH];
 #pragma unroll
-    for (int i = 0; i < D; ++i) {
-      so[i] = s[i];
-      si[i] = s[D + i];
-      ao[i] = fdeg * c_w[W + C::OFF_B2O + i];
-      ai[i] = fdeg * c_w[W + C::OFF_B2I + i];
+    for (int j = 0; j < NPH; ++j) u[j] = cpair(W + C::OFF_BP1 + 2 * j);
+    {
+      float hc[D + 2];
+#pragma unroll
+      for (int i = 0; i < D; ++i) hc[i] = hin[i];
+      hc[D] = cn;
+      hc[D + 1] = static_cast<float>(deg[nn]);
+      mv2<D + 2, NPH, C::OFF_WU, C::DP>(W, hc, u);
+      float sv[2 * D];
+#pragma unroll
+      for (int j = 0; j < NP2; ++j) {
+        sv[2 * j] = s[j].x;
+        sv[2 * j + 1] = s[j].y;
+      }
+      mv2<2 * D, NPH, C::OFF_WU + (D + 2) * C::DP, C::DP>(W, sv, u);
     }
-    matvec_acc<D, D, W + C::OFF_W2O, C::DP>(so, ao);
-    matvec_acc<D, D, W + C::OFF_W2I, C::DP>(si, ai);
+    float uv[D];
 #pragma unroll
-    for (int i = 0; i < D; ++i) {
-      x[i] = h[i];
-      x[D + 1 + i] = ao[i];
-      x[2 * D + 1 + i] = ai[i];
+    for (int j = 0; j < NPH; ++j) {
+      const float2 r2 = relu2x(u[j]);
+      if (2 * j < D) uv[2 * j] = r2.x;
+      if (2 * j + 1 < D) uv[2 * j + 1] = r2.y;
     }
-    x[D] = cn;
-    // psi: u = relu(x . Wp1 + bp1); o = u . Wp2 + bp2; h += alpha * o
-    float u[D], o[D];
+    float2 o[NPH];
 #pragma unroll
-    for (int i = 0; i < D; ++i) {
-      u[i] = c_w[W + C::OFF_BP1 + i];
-      o[i] = c_w[W + C::OFF_BP2 + i];
+    for (int j = 0; j < NPH; ++j) o[j] = cpair(W + C::OFF_BP2 + 2 * j);
+    mv2<D, NPH, C::OFF_WP2, C::DP>(W, uv, o);
+    float hn[C::DH];
+    float2 fin = make_float2(0.f, 0.f);
+    const float2 al = bcast(alpha);
+#pragma unroll
+    for (int j = 0; j < NPH; ++j) {
+      float2 hp = make_float2(hin[2 * j], 2 * j + 1 < D ? hin[2 * j + 1] : 0.f);
+      hp = ffma2(al, o[j], hp);
+      fin = ffma2(hp, make_float2(0.f, 0.f), fin);  // NaN iff some h is non-finite (dss.py:324)
+      hn[2 * j] = hp.x;
+      hn[2 * j + 1] = (2 * j + 1 < D) ? hp.y : 0.f;
     }
-    matvec_acc<3 * D + 1, D, W + C::OFF_WP1, C::DP>(x, u);
-#pragma unroll
-    for (int i = 0; i < D; ++i) u[i] = relu_nan(u[i]);
-    matvec_acc<D, D, W + C::OFF_WP2, C::DP>(u, o);
-    float fin = 0.f;
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-      h[i] = fmaf(alpha, o[i], h[i]);
-      fin = fmaf(h[i], 0.f, fin);  // NaN iff some h[i] is non-finite (dss.py:324)
-    }
-    if (fin != 0.f && first_bad == 0) first_bad = layer_no;
-    store_h<D>(ns.h + n * C::HS, h);
+    // lanes past k write the dummy h row k (branch-free, see phase A)
+    if ((fin.x != 0.f || fin.y != 0.f) && first_bad == 0 && n < k) first_bad = layer_no;
+    store_vec<C::DH>(ns.h + min(n, k) * C::HS, hn);
   }
   if (first_bad != 0 && *bad == 0) *bad = first_bad;
   __syncthreads();
 }
-
-template <int D, int L, int MODE>
-struct LayerLoop {
-  __device__ __forceinline__ static void run(int nl, int k, float* gq, float* gh, float* gc,
-                                             const float4* edges, const int* slice_off,
-                                             const uint16_t* deg, float alpha, int* bad,
-                                             int layer0) {
-    if constexpr (L < Cfg<D>::LMAX) {
-      if (L < nl) {
-        gnn_layer<D, L, MODE>(k, gq, gh, gc, edges, slice_off, deg, alpha, bad, layer0 + L);
-        LayerLoop<D, L + 1, MODE>::run(nl, k, gq, gh, gc, edges, slice_off, deg, alpha, bad,
-                                     layer0);
-      }
-    }
-  }
-};
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -265,14 +285,15 @@ struct GnnShared {
   double scale;
 };
 
-template <int D, int MODE>
+template <int D, int MODE, bool SLOTS>
 __device__ __forceinline__ void gnn_body(const GnnArgs& a, GnnShared& sh, int sub, int pos0,
                                          int k) {
   using C = Cfg<D>;
   constexpr bool SV = MODE == 0;  // node state fully in shared memory
   const int tid = threadIdx.x, nthr = blockDim.x;
-  float* gq = MODE == 2 ? a.qbuf + static_cast<size_t>(pos0) * C::QS : nullptr;
-  float* gh = MODE >= 1 ? a.hbuf + static_cast<size_t>(pos0) * C::HS : nullptr;
+  // global Q scratch keeps one extra (dummy) row per subdomain
+  float* gq = MODE == 2 ? a.qbuf + static_cast<size_t>(pos0 + sub) * C::QS : nullptr;
+  float* gh = MODE >= 1 ? a.hbuf + static_cast<size_t>(pos0 + sub) * C::HS : nullptr;
   float* gc = MODE >= 1 ? a.cbuf + pos0 : nullptr;
   NodeState<D, MODE> ns(k, gq, gh, gc);
   double (&red)[2][kGnnThreads / 32] = sh.red;
@@ -311,7 +332,7 @@ __device__ __forceinline__ void gnn_body(const GnnArgs& a, GnnShared& sh, int su
       a.r0r[sub] = t1;
     }
     __syncthreads();
-    s = sh_scale;
+    s = __shfl_sync(0xffffffffu, sh_scale, 0);
     if (s == 0.0) {  // zero local residual: the subdomain contributes nothing
       if (tid == 0) {
         a.bad_layer[sub] = 0;
@@ -326,49 +347,78 @@ __device__ __forceinline__ void gnn_body(const GnnArgs& a, GnnShared& sh, int su
     }
     __syncthreads();  // scratch (aliasing Q) fully consumed
     for (int n = tid; n < k; n += nthr) {
-      float z[D];
+      float z[C::DH];
 #pragma unroll
-      for (int i = 0; i < D; ++i) z[i] = 0.f;
-      store_h<D>(ns.h + n * C::HS, z);
+      for (int i = 0; i < C::DH; ++i) z[i] = 0.f;
+      store_vec<C::DH>(ns.h + n * C::HS, z);
     }
   } else {
-    s = a.scale[sub];
+    s = __shfl_sync(0xffffffffu, a.scale[sub], 0);
     if (s == 0.0) return;
     if constexpr (SV) {
       for (int n = tid; n < k; n += nthr) {
         ns.c[n] = a.cbuf[pos0 + n];
-        float hv[D];
-        load_h<D>(a.hbuf + static_cast<size_t>(pos0 + n) * C::HS, hv);
-        store_h<D>(ns.h + n * C::HS, hv);
+        float hv[C::DH];
+        load_vec<C::DH>(a.hbuf + static_cast<size_t>(pos0 + sub + n) * C::HS, hv);
+        store_vec<C::DH>(ns.h + n * C::HS, hv);
       }
     }
   }
+  // dummy Q row k: target of the SELL padding records (2 relu(P - 1e30) == 0)
+  for (int j = tid; j < C::QS; j += nthr) ns.q[static_cast<size_t>(k) * C::QS + j] = -1e30f;
   __syncthreads();
 
-  LayerLoop<D, 0, MODE>::run(a.nl, k, gq, gh, gc, a.edges, a.slice_off + a.slice_base[sub],
-                           a.deg + pos0, a.alpha, &sh_bad, a.layer0);
+  {
+    const int warp = uni(tid >> 5);
+    const float2* xy = a.xy + pos0;
+    const int* so = a.slice_off + a.slice_base[sub];
+    const uint16_t* dg = a.deg + pos0;
+    if constexpr (SLOTS) {
+      // compile-time bank slots (LMAX <= 10)
+#define DDM_LAYER(LL)                                                                        \
+  if constexpr (LL < C::LMAX) {                                                              \
+    if (LL < a.nl)                                                                           \
+      gnn_layer<D, MODE, LL * C::STRIDE>(0, k, warp, gq, gh, gc, xy, a.edges, so, dg, a.alpha, \
+                                         &sh_bad, a.layer0 + LL);                            \
+  }
+      DDM_LAYER(0) DDM_LAYER(1) DDM_LAYER(2) DDM_LAYER(3) DDM_LAYER(4)
+      DDM_LAYER(5) DDM_LAYER(6) DDM_LAYER(7) DDM_LAYER(8) DDM_LAYER(9)
+#undef DDM_LAYER
+    } else {
+#pragma unroll 1
+      for (int l = 0; l < a.nl; ++l)
+        gnn_layer<D, MODE, -1>(l * C::STRIDE, k, warp, gq, gh, gc, xy, a.edges, so, dg, a.alpha,
+                               &sh_bad, a.layer0 + l);
+    }
+  }
 
   int outbad = 0;
   if (a.last) {
     // ---- decoder of the final layer (dss.py:327) and rescaling (hybrid.py:135) ----
     for (int n = tid; n < k; n += nthr) {
+      float hv[C::DH];
+      load_vec<C::DH>(ns.h + n * C::HS, hv);
       float h[D];
-      load_h<D>(ns.h + n * C::HS, h);
-      float u[D];
 #pragma unroll
-      for (int i = 0; i < D; ++i) u[i] = c_w[C::DEC_B1 + i];
-      matvec_acc<D, D, C::DEC_W1, C::DP>(h, u);
+      for (int i = 0; i < D; ++i) h[i] = hv[i];
+      float2 u[C::NPH];
+#pragma unroll
+      for (int j = 0; j < C::NPH; ++j) u[j] = cpair(C::DEC_B1 + 2 * j);
+      mv2<D, C::NPH, C::DEC_W1, C::DP>(0, h, u);
       float o = c_w[C::DEC_B2];
 #pragma unroll
-      for (int i = 0; i < D; ++i) o = fmaf(relu_nan(u[i]), c_w[C::DEC_W2 + i], o);
+      for (int i = 0; i < D; ++i) {
+        const float ui = (i & 1) ? u[i >> 1].y : u[i >> 1].x;
+        o = fmaf(relu_nan(ui), c_w[C::DEC_W2 + i], o);
+      }
       if (!isfinite(o)) outbad = 1;
       a.zloc[pos0 + n] = s * static_cast<double>(o);
     }
   } else if constexpr (SV) {
     for (int n = tid; n < k; n += nthr) {
-      float hv[D];
-      load_h<D>(ns.h + n * C::HS, hv);
-      store_h<D>(a.hbuf + static_cast<size_t>(pos0 + n) * C::HS, hv);
+      float hv[C::DH];
+      load_vec<C::DH>(ns.h + n * C::HS, hv);
+      store_vec<C::DH>(a.hbuf + static_cast<size_t>(pos0 + sub + n) * C::HS, hv);
     }
   }
   outbad = __syncthreads_or(outbad);
@@ -385,22 +435,32 @@ __device__ __forceinline__ void gnn_body(const GnnArgs& a, GnnShared& sh, int su
   }
 }
 
-// One CTA per subdomain (LPT order); the node-state placement is chosen per CTA:
-// a.cap0 = largest k with h, Q, c in the launch's shared memory, a.cap1 = largest
-// k with Q alone in shared memory.
+// Subdomains whose node state (h, Q, c) fits the launch's shared memory (k <=
+// a.cap0): one CTA per subdomain in LPT order, compile-time bank slots.
 template <int D>
 __global__ void __launch_bounds__(kGnnThreads, 1) gnn_kernel(GnnArgs a) {
-  if (a.skip != nullptr && *a.skip != 0) return;
+  if (a.skip != nullptr && uni(*a.skip) != 0) return;
   __shared__ GnnShared sh;
-  const int sub = a.order[a.order_begin + blockIdx.x];
-  const int pos0 = a.sub_ptr[sub];
-  const int k = a.sub_ptr[sub + 1] - pos0;
-  if (k <= a.cap0) {
-    gnn_body<D, 0>(a, sh, sub, pos0, k);
-  } else if (k <= a.cap1) {
-    gnn_body<D, 1>(a, sh, sub, pos0, k);
+  const int sub = uni(a.order[a.order_begin + blockIdx.x]);
+  const int pos0 = uni(a.sub_ptr[sub]);
+  const int k = uni(a.sub_ptr[sub + 1] - pos0);
+  gnn_body<D, 0, true>(a, sh, sub, pos0, k);
+}
+
+// The few oversized subdomains (k > a.cap0): Q alone in shared memory (k <= a.cap1,
+// compile-time bank slots) or everything in global scratch (runtime bank slots).  Launched concurrently with
+// gnn_kernel on a side stream (gnn.cu).
+template <int D>
+__global__ void __launch_bounds__(kGnnThreads, 1) gnn_big_kernel(GnnArgs a) {
+  if (a.skip != nullptr && uni(*a.skip) != 0) return;
+  __shared__ GnnShared sh;
+  const int sub = uni(a.order[a.order_begin + blockIdx.x]);
+  const int pos0 = uni(a.sub_ptr[sub]);
+  const int k = uni(a.sub_ptr[sub + 1] - pos0);
+  if (k <= a.cap1) {
+    gnn_body<D, 1, true>(a, sh, sub, pos0, k);
   } else {
-    gnn_body<D, 2>(a, sh, sub, pos0, k);
+    gnn_body<D, 2, false>(a, sh, sub, pos0, k);
   }
 }
 

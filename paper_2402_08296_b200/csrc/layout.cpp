@@ -18,6 +18,7 @@
 #include <numeric>
 
 #include "ddmgnn_internal.h"
+#include "gnn_cfg.h"
 
 namespace ddmgnn {
 
@@ -135,18 +136,44 @@ int build_host_layout(int n, const int64_t* indptr, const int32_t* indices, cons
   L.slice_off[S] = static_cast<int>(off);
   L.E = E;
   L.E_pad = off;
-  L.edges.assign(static_cast<size_t>(off) * 4, 0.f);
+  L.edges.assign(static_cast<size_t>(off) * 2, 0.f);
+  L.xy.assign(2ull * L.V, 0.f);
 
-  // ---- pass 2: edge records {dx, dy, |d|, dst} (dss.py:177-185) ----
+  // ---- pass 2: edge records {|d|, dst} (dss.py:177-185) and centred coordinates ----
+  // edge_vec = coords[dst] - coords[src] (dss.py:184) enters the model only
+  // linearly (W1cat rows 2d, 2d+1), so the kernel folds it into the per-node
+  // projections; the node coordinates are stored relative to the subdomain's
+  // bounding-box centre so the fp32 difference keeps ~1e-6 relative accuracy.
 #pragma omp parallel
   {
     std::vector<int> loc(n, -1);
 #pragma omp for schedule(dynamic, 4)
     for (int i = 0; i < K; ++i) {
       const int b = L.sub_ptr[i], e = L.sub_ptr[i + 1];
-      for (int p = b; p < e; ++p) loc[L.idx[p]] = p - b;
+      double lo[2] = {HUGE_VAL, HUGE_VAL}, hi[2] = {-HUGE_VAL, -HUGE_VAL};
+      for (int p = b; p < e; ++p) {
+        const int g = L.idx[p];
+        loc[g] = p - b;
+        for (int a = 0; a < 2; ++a) {
+          lo[a] = std::min(lo[a], coords[2 * g + a]);
+          hi[a] = std::max(hi[a], coords[2 * g + a]);
+        }
+      }
+      const double cx = 0.5 * (lo[0] + hi[0]), cy = 0.5 * (lo[1] + hi[1]);
+      // padding records (SELL slots past a node's degree, lanes past k) point at the
+      // kernel's dummy Q row k with |d| = 0
+      {
+        const int kk = e - b, ns = (kk + 31) / 32;
+        const long long r0 = L.slice_off[L.slice_base[i]], r1 = L.slice_off[L.slice_base[i] + ns];
+        for (long long r = r0; r < r1; ++r) {
+          L.edges[2 * r] = 0.f;
+          std::memcpy(&L.edges[2 * r + 1], &kk, 4);
+        }
+      }
       for (int p = b; p < e; ++p) {
         const int a = p - b, g = L.idx[p];
+        L.xy[2ull * p] = static_cast<float>(coords[2 * g] - cx);
+        L.xy[2ull * p + 1] = static_cast<float>(coords[2 * g + 1] - cy);
         const long long base = L.slice_off[L.slice_base[i] + (a >> 5)] + (a & 31);
         int slot = 0;
         for (long long jj = indptr[g]; jj < indptr[g + 1]; ++jj) {
@@ -154,13 +181,10 @@ int build_host_layout(int n, const int64_t* indptr, const int32_t* indices, cons
           if (c == g || loc[c] < 0) continue;
           const double dx = coords[2 * c] - coords[2 * g];
           const double dy = coords[2 * c + 1] - coords[2 * g + 1];
-          const double len = std::hypot(dx, dy);
-          float* rec = &L.edges[static_cast<size_t>(base + 32ll * slot) * 4];
-          rec[0] = static_cast<float>(dx);
-          rec[1] = static_cast<float>(dy);
-          rec[2] = static_cast<float>(len);
+          float* rec = &L.edges[static_cast<size_t>(base + 32ll * slot) * 2];
+          rec[0] = static_cast<float>(std::hypot(dx, dy));
           int dst = loc[c];
-          std::memcpy(&rec[3], &dst, 4);
+          std::memcpy(&rec[1], &dst, 4);
           ++slot;
         }
       }
@@ -194,19 +218,27 @@ int build_host_layout(int n, const int64_t* indptr, const int32_t* indices, cons
 
 // Pack the reference's flat float64 parameters (dss.py:93-99 order: per layer
 // phi_out, phi_in, psi, dec, each (w1, b1, w2, b2)) into fp32 constant banks.
-// Per-layer bank layout (gnn_cfg.h, rows padded to 4 floats):
-//   Wsrc[D][2D] Wdst[D][2D] We[3][2D] b1cat[2D]   rows of W1cat (dss.py:281-290,
-//                                                  in-MLP dx,dy rows negated)
-//   W2o[D][D] b2o[D] W2i[D][D] b2i[D] Wp1[3D+1][D] bp1[D] Wp2[D][D] bp2[D]
-// and the FINAL layer's decoder (dss.py:327; only the last output is consumed by
-// hybrid.py:124) at the end of every bank: Wd1[D][D] bd1[D] wd2[D] bd2.
+// Per-layer bank layout (gnn_cfg.h, rows padded to 4 floats); W1cat is the
+// reference's stacked hidden layer of both message MLPs (dss.py:281-290, the
+// in-MLP's dx,dy rows negated), rows [h_src (d), h_dst (d), dx, dy, |d|]:
+//   WQ  [d+2][2d]  = [W1cat h_dst rows ; +W1cat dx row ; +W1cat dy row]
+//   WP  [d+2][2d]  = [W1cat h_src rows ; -W1cat dx row ; -W1cat dy row]
+//   b1  [2d], WL [2d] = W1cat |d| row
+//   WU  [3d+2][d]  = [Wp1 h rows ; Wp1 c row ; bdeg ; Mo ; Mi]
+//         bdeg = b2o . Wp1[phi_o rows] + b2i . Wp1[phi_i rows]      (x node degree)
+//         Mo   = 0.5 * W2o . Wp1[phi_o rows],  Mi = 0.5 * W2i . Wp1[phi_i rows]
+//   bp1 [d], WP2 [d][d] = 0.5 * Wp2, bp2 [d]
+// (the 0.5 factors pair with the kernel's relu(x) = (x + |x|) / 2).  The folded
+// products are formed in fp64 and rounded once.  The FINAL layer's decoder
+// (dss.py:327; only the last output is consumed by hybrid.py:124) sits at the end
+// of every bank: Wd1[d][d] bd1[d] wd2[d] bd2.
 int pack_model(int k_bar, int d, double alpha, const double* params, long long n_params,
                PackedModel* out, std::string* err) {
   if (k_bar < 1 || d < 1) {
     *err = "k_bar and d must be >= 1";
     return kValueError;
   }
-  int o[20];
+  int o[kBankOffsets];
   if (!gnn_bank_offsets(d, o)) {
     *err = "latent dimension d=" + std::to_string(d) +
            " has no compiled kernel (supported: 3, 4, 10)";
@@ -219,8 +251,7 @@ int pack_model(int k_bar, int d, double alpha, const double* params, long long n
            std::to_string(n_params * 8);
     return kValueError;
   }
-  enum { WSRC, WDST, WE, B1, W2O, B2O, W2I, B2I, WP1, BP1, WP2, BP2, STRIDE, D2P, DP, DW1, DB1,
-         DW2, DB2, LMAX };
+  enum { WQ, WP, B1, WL, WU, BP1, WP2, BP2, STRIDE, D2P, DP, DW1, DB1, DW2, DB2, LMAX };
   const int D = d;
   const int lmax = o[LMAX], stride = o[STRIDE], d2p = o[D2P], dp = o[DP];
   PackedModel& M = *out;
@@ -235,6 +266,7 @@ int pack_model(int k_bar, int d, double alpha, const double* params, long long n
 
   const double* p = params;
   const double* last_dec = nullptr;
+  auto f = [](double v) { return static_cast<float>(v); };
   for (int l = 0; l < k_bar; ++l) {
     const double* w1o = p; p += (2 * D + 3) * D;
     const double* b1o = p; p += D;
@@ -257,30 +289,40 @@ int pack_model(int k_bar, int d, double alpha, const double* params, long long n
       if (row == 2 * D || row == 2 * D + 1) v = -v;
       return v;
     };
-    auto f = [](double v) { return static_cast<float>(v); };
-    for (int m = 0; m < D; ++m)
-      for (int j = 0; j < 2 * D; ++j) {
-        B[o[WSRC] + m * d2p + j] = f(w1cat(m, j));
-        B[o[WDST] + m * d2p + j] = f(w1cat(D + m, j));
+    for (int j = 0; j < 2 * D; ++j) {
+      for (int m = 0; m < D; ++m) {
+        B[o[WQ] + m * d2p + j] = f(w1cat(D + m, j));
+        B[o[WP] + m * d2p + j] = f(w1cat(m, j));
       }
-    for (int r = 0; r < 3; ++r)
-      for (int j = 0; j < 2 * D; ++j) B[o[WE] + r * d2p + j] = f(w1cat(2 * D + r, j));
+      for (int a = 0; a < 2; ++a) {
+        B[o[WQ] + (D + a) * d2p + j] = f(w1cat(2 * D + a, j));
+        B[o[WP] + (D + a) * d2p + j] = f(-w1cat(2 * D + a, j));
+      }
+      B[o[B1] + j] = f(j < D ? b1o[j] : b1i[j - D]);
+      B[o[WL] + j] = f(w1cat(2 * D + 2, j));
+    }
+    // psi first layer (3D+1 inputs [h, c, phi_o, phi_i], dss.py:293-299) with the
+    // messages' second layer folded in
+    const double* wp1_o = wp1 + (D + 1) * D;      // rows of phi_o
+    const double* wp1_i = wp1 + (2 * D + 1) * D;  // rows of phi_i
     for (int j = 0; j < D; ++j) {
-      B[o[B1] + j] = f(b1o[j]);
-      B[o[B1] + D + j] = f(b1i[j]);
-      B[o[B2O] + j] = f(b2o[j]);
-      B[o[B2I] + j] = f(b2i[j]);
+      for (int m = 0; m <= D; ++m) B[o[WU] + m * dp + j] = f(wp1[m * D + j]);  // h rows, c row
+      double bd = 0.0;
+      for (int q = 0; q < D; ++q) bd += b2o[q] * wp1_o[q * D + j] + b2i[q] * wp1_i[q * D + j];
+      B[o[WU] + (D + 1) * dp + j] = f(bd);
+      for (int m = 0; m < D; ++m) {
+        double mo = 0.0, mi = 0.0;
+        for (int q = 0; q < D; ++q) {
+          mo += w2o[m * D + q] * wp1_o[q * D + j];
+          mi += w2i[m * D + q] * wp1_i[q * D + j];
+        }
+        B[o[WU] + (D + 2 + m) * dp + j] = f(0.5 * mo);
+        B[o[WU] + (2 * D + 2 + m) * dp + j] = f(0.5 * mi);
+      }
       B[o[BP1] + j] = f(bp1[j]);
       B[o[BP2] + j] = f(bp2[j]);
+      for (int m = 0; m < D; ++m) B[o[WP2] + m * dp + j] = f(0.5 * wp2[m * D + j]);
     }
-    for (int m = 0; m < D; ++m)
-      for (int j = 0; j < D; ++j) {
-        B[o[W2O] + m * dp + j] = f(w2o[m * D + j]);
-        B[o[W2I] + m * dp + j] = f(w2i[m * D + j]);
-        B[o[WP2] + m * dp + j] = f(wp2[m * D + j]);
-      }
-    for (int m = 0; m < 3 * D + 1; ++m)
-      for (int j = 0; j < D; ++j) B[o[WP1] + m * dp + j] = f(wp1[m * D + j]);
   }
   // decoder of the final layer: w1 [D][D], b1 [D], w2 [D][1], b2 [1]
   const double* dw1 = last_dec;
