@@ -110,6 +110,38 @@ int ddmgnn_pcg_host_precond(ddmgnn_ctx* ctx, const double* b, const double* u0, 
                             double tol, int max_iter, ddmgnn_host_precond_fn fn, void* user,
                             int* iterations, double* history, int* converged);
 
+/* ---- Sharded solve building blocks (one process per GPU) ----
+ * A rank's context holds its group of subdomains over its local DOF set; the
+ * host issues the collectives between these stream-ordered calls
+ * (paper_2402_08296_b200/sharded.py).  All pointers are device pointers. */
+/* Device buffers filled by ddmgnn_launch_gnn_only: zloc[V] = s_i * DSS output of
+ * every batched node (hybrid.py:135), scale[K] = s_i (hybrid.py:105), r0r[K] =
+ * (R0 r)_i (hybrid.py:117).  Any output pointer may be NULL. */
+int ddmgnn_local_outputs(ddmgnn_ctx* ctx, double** zloc, double** scale, double** r0r);
+/* Replace the partition-of-unity weights 1/multiplicity (decomp.py:184-190) that
+ * build derived from the context's own subdomains — a shard passes the weights of
+ * the global decomposition restricted to its local DOF set (length n). */
+int ddmgnn_set_pou(ddmgnn_ctx* ctx, int64_t n, const double* pou);
+/* dst[i] = src[idx[i]] and dst[idx[i]] = src[i], i < n (halo pack / unpack). */
+int ddmgnn_gather(const double* src, const int32_t* idx, int64_t n, double* dst, void* stream);
+int ddmgnn_scatter(const double* src, const int32_t* idx, int64_t n, double* dst, void* stream);
+/* *out = x . y (fixed two-stage order; work holds >= 1184 doubles). */
+int ddmgnn_dot(int64_t n, const double* x, const double* y, double* work, double* out,
+               void* stream);
+/* u += alpha p, r -= alpha q (sparse.py:112-113), *rr_out = r . r (sparse.py:114). */
+int ddmgnn_axpy2(int64_t n, double alpha, const double* p, const double* q, double* u, double* r,
+                 double* work, double* rr_out, void* stream);
+/* p = z + beta p (sparse.py:126). */
+int ddmgnn_xpby(int64_t n, const double* z, double beta, double* p, void* stream);
+/* y = A x, A dense row-major k x k (the coarse inverse, sparse.py:163 / hybrid.py:117). */
+int ddmgnn_dense_gemv(int64_t k, const double* a, const double* x, double* y, void* stream);
+/* Gluing over a transpose map (hybrid.py:117,133-135): for DOF j < n,
+ * z_j = [two_level] sum_t pou_j y[sub_t] + sum_{t: scale[sub_t] != 0} zloc[pos_t],
+ * t in [tptr[j], tptr[j+1]) ascending subdomain; tent = int32 pairs (pos, sub). */
+int ddmgnn_prolong(int64_t n, int two_level, const int32_t* tptr, const int32_t* tent,
+                   const double* pou, const double* y, const double* scale, const double* zloc,
+                   double* z, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -59,6 +59,16 @@ SIGNATURES = [
     ("ddmgnn_pcg", _int, [_ctx, _vp, _vp, _vp, _dbl, _int, _int, _int, _vp, _pint, _pd, _pint]),
     ("ddmgnn_pcg_host_precond", _int,
      [_ctx, _pd, _pd, _pd, _dbl, _int, HOST_PRECOND_FN, _vp, _pint, _pd, _pint]),
+    ("ddmgnn_local_outputs", _int, [_ctx, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                                    ctypes.POINTER(_vp)]),
+    ("ddmgnn_set_pou", _int, [_ctx, _i64, _pd]),
+    ("ddmgnn_gather", _int, [_vp, _vp, _i64, _vp, _vp]),
+    ("ddmgnn_scatter", _int, [_vp, _vp, _i64, _vp, _vp]),
+    ("ddmgnn_dot", _int, [_i64, _vp, _vp, _vp, _vp, _vp]),
+    ("ddmgnn_axpy2", _int, [_i64, _dbl, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    ("ddmgnn_xpby", _int, [_i64, _vp, _dbl, _vp, _vp]),
+    ("ddmgnn_dense_gemv", _int, [_i64, _vp, _vp, _vp, _vp]),
+    ("ddmgnn_prolong", _int, [_i64, _int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
 ]
 
 _lib = None
@@ -198,6 +208,17 @@ class Context:
 
     def launch_gnn_only(self, r_ptr: int, stream: int = 0):
         check(self._lib.ddmgnn_launch_gnn_only(self._h, _vp(r_ptr), _vp(stream or None)))
+
+    def set_pou(self, pou):
+        w = np.ascontiguousarray(pou, dtype=np.float64)
+        check(self._lib.ddmgnn_set_pou(self._h, w.size, dptr(w)))
+
+    def local_outputs(self):
+        """Device pointers (zloc, scale, r0r) written by launch_gnn_only."""
+        z, s, r = _vp(), _vp(), _vp()
+        check(self._lib.ddmgnn_local_outputs(self._h, ctypes.byref(z), ctypes.byref(s),
+                                             ctypes.byref(r)))
+        return z.value, s.value, r.value
 
     def spmv_device(self, x_ptr: int, y_ptr: int, stream: int = 0):
         check(self._lib.ddmgnn_spmv(self._h, _vp(x_ptr), _vp(y_ptr), _vp(stream or None)))

@@ -33,6 +33,13 @@ static int fail(int code, const std::string& msg) {
   return code;
 }
 
+namespace ddmgnn {
+int report_cuda(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return kOk;
+  return fail(kCudaError, std::string("CUDA error: ") + cudaGetErrorString(e) + " (" + what + ")");
+}
+}  // namespace ddmgnn
+
 #define CUDA_TRY(expr)                                                                     \
   do {                                                                                     \
     cudaError_t _e = (expr);                                                               \
@@ -574,6 +581,25 @@ extern "C" int ddmgnn_launch_gnn_only(ddmgnn_ctx* c, const double* r, void* stre
   if (st) return st;
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(enqueue_gnn(c, r, c->d_status, nullptr, pick(c, stream)));
+  return kOk;
+}
+
+extern "C" int ddmgnn_set_pou(ddmgnn_ctx* c, int64_t n, const double* pou) {
+  if (!c || !c->built) return fail(kStateError, "build must be called first");
+  if (n != c->n) return fail(kValueError, "expected pou of length " + std::to_string(c->n));
+  for (int64_t j = 0; j < n; ++j)
+    if (!(pou[j] > 0.0)) return fail(kValueError, "pou weights must be positive");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaMemcpy(c->lay.pou, pou, sizeof(double) * n, cudaMemcpyHostToDevice));
+  return kOk;
+}
+
+extern "C" int ddmgnn_local_outputs(ddmgnn_ctx* c, double** zloc, double** scale,
+                                    double** r0r) {
+  if (!c || !c->built) return fail(kStateError, "build must be called first");
+  if (zloc) *zloc = c->d_zloc;
+  if (scale) *scale = c->d_scale;
+  if (r0r) *r0r = c->d_r0r;
   return kOk;
 }
 

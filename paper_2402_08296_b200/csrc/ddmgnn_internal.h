@@ -49,7 +49,8 @@ enum DevStatus : int {
   kPrecondError = 5,
 };
 
-constexpr int kGnnThreads = 512;
+constexpr int kGnnThreads = 512;  // max CTA size (big-subdomain kernel)
+constexpr int kGnnNpt = 1;        // nodes per thread of the main GNN kernel (CTA = 512 / kGnnNpt)
 constexpr int kConstFloats = 16384;  // 64 KB constant bank
 constexpr int kGnnSmemMax = 227 * 1024 - 1024;  // dynamic smem cap (static smem < 1 KB)
 
@@ -137,6 +138,9 @@ size_t gnn_plan_smem(int d, int k_max, int* cap0, int* cap1);
 cudaError_t launch_gnn(int d, int n_ctas, int n_big, int k_max, int k_max_small, size_t smem,
                        const GnnArgs& a, cudaStream_t s, cudaStream_t side, cudaEvent_t fork,
                        cudaEvent_t join);
+
+// capi.cu: record a CUDA failure as the thread's last error; returns the status code
+int report_cuda(cudaError_t e, const char* what);
 
 // krylov.cu
 struct PcgState {

@@ -39,8 +39,13 @@ cudaError_t DDM_NAME(gnn_upload)(const float* dev_bank, cudaStream_t s) {
 // subdomain of the launch, smem = dynamic shared memory chosen by the host.
 cudaError_t DDM_NAME(gnn_launch)(int n_ctas, int k_max, size_t smem, const GnnArgs& a,
                                  cudaStream_t s) {
-  int threads = ((k_max + 31) / 32) * 32;
-  if (threads > kGnnThreads) threads = kGnnThreads;
+#ifdef GNN_BIG
+  const int cap = kGnnThreads, npt = 1;
+#else
+  const int cap = kGnnThreads / kGnnNpt, npt = kGnnNpt;
+#endif
+  int threads = ((k_max + 32 * npt - 1) / (32 * npt)) * 32;
+  if (threads > cap) threads = cap;
   if (threads < 64) threads = 64;
   DDM_KERNEL<GNN_D><<<n_ctas, threads, smem, s>>>(a);
   return cudaGetLastError();

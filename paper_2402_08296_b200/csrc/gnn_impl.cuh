@@ -105,6 +105,21 @@ __device__ __forceinline__ void mv2(int base, const float (&x)[NIN], float2 (&ac
   }
 }
 
+// The same for NPT nodes at once: every weight pair (one LDCU) feeds NPT FFMA2.
+template <int NPT, int NIN, int NPO, int OFF, int RS>
+__device__ __forceinline__ void mv2n(int base, const float (&x)[NPT][NIN],
+                                     float2 (&acc)[NPT][NPO]) {
+#pragma unroll
+  for (int m = 0; m < NIN; ++m) {
+#pragma unroll
+    for (int j = 0; j < NPO; ++j) {
+      const float2 w = cpair(base + OFF + m * RS + 2 * j);
+#pragma unroll
+      for (int t = 0; t < NPT; ++t) acc[t][j] = ffma2(bcast(x[t][m]), w, acc[t][j]);
+    }
+  }
+}
+
 // [h (D), x, y] of a node: h from the node state, (x, y) subdomain-centred coordinates.
 template <int D>
 __device__ __forceinline__ void load_hxy(const float* hrow, float2 xy, float (&v)[D + 2]) {
@@ -152,11 +167,16 @@ __device__ __forceinline__ int uni(int v) { return __shfl_sync(0xffffffffu, v, 0
 // One message-passing layer for the CTA's subdomain.  WT >= 0: the layer's slot
 // offset in the constant bank as a compile-time constant (every weight pair is an
 // immediate-addressed LDCU.128 feeding FFMA2 — the fast path); WT < 0: runtime
-// offset w_rt (used only by the rare big-subdomain kernel).  Node loops run a uniform trip count: warp w of the
-// CTA handles local nodes n0 + lane, n0 = it * nthr + 32 w, i.e. exactly SELL slice
-// n0 / 32, whose width (max degree in the slice) bounds the edge loop.  Padding
-// records point at the dummy Q row k (all -1e30), whose 2 relu term is exactly 0.
-template <int D, int MODE, int WT>
+// offset w_rt (used only by the rare big-subdomain kernel).
+//
+// Node loops run a uniform trip count: each warp handles NPT consecutive SELL
+// slices (32 local nodes each) per iteration, node t of lane = n0 + 32 t + lane,
+// so one weight load feeds NPT nodes.  Slice widths (max degree in the slice)
+// bound the edge loop; padding records point at the dummy Q row k (all -1e30),
+// whose 2 relu term is exactly 0.  Lanes past k recompute node k-1 (phase A,
+// identical store) or write the dummy h row k (phase B): no divergent branches,
+// so the weight loads stay uniform.
+template <int D, int MODE, int WT, int NPT>
 __device__ __forceinline__ void gnn_layer(int w_rt, int k, int warp, float* gq, float* gh,
                                           float* gc, const float2* __restrict__ xy,
                                           const float2* __restrict__ edges,
@@ -167,107 +187,148 @@ __device__ __forceinline__ void gnn_layer(int w_rt, int k, int warp, float* gq, 
   const int W = WT >= 0 ? WT : w_rt;
   constexpr int NP2 = C::NP2, NPH = C::NPH;
   const int lane = threadIdx.x & 31, nthr = blockDim.x;
+  const int step = NPT * nthr;
   NodeState<D, MODE> ns(k, gq, gh, gc);
   // ---- phase A: destination projections Q_t = [h_t, x_t, y_t] . WQ ----
-  for (int n0 = 32 * warp; n0 < k; n0 += nthr) {
-    const int n = n0 + lane;
-    const int nn = min(n, k - 1);
-    float hin[D + 2];
-    load_hxy<D>(ns.h + nn * C::HS, __ldg(xy + nn), hin);
-    float2 q[NP2];
+  for (int n0 = 32 * NPT * warp; n0 < k; n0 += step) {
+    float hin[NPT][D + 2];
+    int nn[NPT];
 #pragma unroll
-    for (int j = 0; j < NP2; ++j) q[j] = make_float2(0.f, 0.f);
-    mv2<D + 2, NP2, C::OFF_WQ, C::D2P>(W, hin, q);
-    float qs[C::QS];
-#pragma unroll
-    for (int j = 0; j < C::QS; ++j) qs[j] = 0.f;
-#pragma unroll
-    for (int j = 0; j < NP2; ++j) {
-      qs[2 * j] = q[j].x;
-      qs[2 * j + 1] = q[j].y;
+    for (int t = 0; t < NPT; ++t) {
+      nn[t] = min(n0 + 32 * t + lane, k - 1);
+      load_hxy<D>(ns.h + nn[t] * C::HS, __ldg(xy + nn[t]), hin[t]);
     }
-    // lanes past k recompute node k-1 and store the identical row: no divergent
-    // branch in the loop, so the weight loads stay uniform (LDCU)
-    store_vec<C::QS>(ns.q + nn * C::QS, qs);
+    float2 q[NPT][NP2];
+#pragma unroll
+    for (int t = 0; t < NPT; ++t)
+#pragma unroll
+      for (int j = 0; j < NP2; ++j) q[t][j] = make_float2(0.f, 0.f);
+    mv2n<NPT, D + 2, NP2, C::OFF_WQ, C::D2P>(W, hin, q);
+#pragma unroll
+    for (int t = 0; t < NPT; ++t) {
+      float qs[C::QS];
+#pragma unroll
+      for (int j = 0; j < C::QS; ++j) qs[j] = 0.f;
+#pragma unroll
+      for (int j = 0; j < NP2; ++j) {
+        qs[2 * j] = q[t][j].x;
+        qs[2 * j + 1] = q[t][j].y;
+      }
+      store_vec<C::QS>(ns.q + nn[t] * C::QS, qs);
+    }
   }
   __syncthreads();
   // ---- phase B: edge aggregation + node update ----
   int first_bad = 0;
-  for (int n0 = 32 * warp; n0 < k; n0 += nthr) {
-    const int n = n0 + lane;
-    const int nn = min(n, k - 1);
-    float hin[D + 2];
-    load_hxy<D>(ns.h + nn * C::HS, __ldg(xy + nn), hin);
-    const float cn = ns.c[nn];
-    float2 p[NP2], s[NP2];
+  const float2 dummy = make_float2(0.f, __int_as_float(k));
+  for (int n0 = 32 * NPT * warp; n0 < k; n0 += step) {
+    int nn[NPT], width[NPT];
+    float2 p[NPT][NP2], s[NPT][NP2];
+    const float2* ep[NPT];
+    {
+      float hin[NPT][D + 2];
 #pragma unroll
-    for (int j = 0; j < NP2; ++j) {
-      p[j] = cpair(W + C::OFF_B1 + 2 * j);
-      s[j] = make_float2(0.f, 0.f);
+      for (int t = 0; t < NPT; ++t) {
+        nn[t] = min(n0 + 32 * t + lane, k - 1);
+        load_hxy<D>(ns.h + nn[t] * C::HS, __ldg(xy + nn[t]), hin[t]);
+#pragma unroll
+        for (int j = 0; j < NP2; ++j) {
+          p[t][j] = cpair(W + C::OFF_B1 + 2 * j);
+          s[t][j] = make_float2(0.f, 0.f);
+        }
+      }
+      mv2n<NPT, D + 2, NP2, C::OFF_WP, C::D2P>(W, hin, p);
     }
-    mv2<D + 2, NP2, C::OFF_WP, C::D2P>(W, hin, p);
-    const int so = uni(slice_off[n0 >> 5]);
-    const int width = (uni(slice_off[(n0 >> 5) + 1]) - so) >> 5;
-    const float2* ep = edges + so + lane;
-    float2 rec = width > 0 ? __ldg(ep) : make_float2(0.f, 0.f);
-    for (int e = 0; e < width; ++e) {
-      const float2 cur = rec;
-      if (e + 1 < width) rec = __ldg(ep + 32 * (e + 1));
-      const int t = __float_as_int(cur.y);
-      float qt[C::QS];
-      load_vec<C::QS>(ns.q + t * C::QS, qt);
-      const float2 len = bcast(cur.x);
+    int wmax = 0;
 #pragma unroll
-      for (int j = 0; j < NP2; ++j) {
-        float2 x = fadd2(p[j], make_float2(qt[2 * j], qt[2 * j + 1]));
-        x = ffma2(len, cpair(W + C::OFF_WL + 2 * j), x);
-        s[j] = fadd2(s[j], relu2x(x));
+    for (int t = 0; t < NPT; ++t) {
+      const int q = (n0 >> 5) + t;
+      const bool live = n0 + 32 * t < k;  // warp-uniform
+      const int so = uni(slice_off[live ? q : 0]);
+      width[t] = live ? (uni(slice_off[q + 1]) - so) >> 5 : 0;
+      ep[t] = edges + so + lane;
+      wmax = max(wmax, width[t]);
+    }
+    float2 rec[NPT];
+#pragma unroll
+    for (int t = 0; t < NPT; ++t) rec[t] = width[t] > 0 ? __ldg(ep[t]) : dummy;
+    for (int e = 0; e < wmax; ++e) {
+      float2 cur[NPT];
+#pragma unroll
+      for (int t = 0; t < NPT; ++t) {
+        cur[t] = rec[t];
+        rec[t] = e + 1 < width[t] ? __ldg(ep[t] + 32 * (e + 1)) : dummy;
+      }
+#pragma unroll
+      for (int t = 0; t < NPT; ++t) {
+        float qt[C::QS];
+        load_vec<C::QS>(ns.q + __float_as_int(cur[t].y) * C::QS, qt);
+        const float2 len = bcast(cur[t].x);
+#pragma unroll
+        for (int j = 0; j < NP2; ++j) {
+          float2 x = fadd2(p[t][j], make_float2(qt[2 * j], qt[2 * j + 1]));
+          x = ffma2(len, cpair(W + C::OFF_WL + 2 * j), x);
+          s[t][j] = fadd2(s[t][j], relu2x(x));
+        }
       }
     }
     // psi first layer with the messages' second layer folded in
-    float2 u[NPH];
+    float2 u[NPT][NPH];
+    float hc[NPT][D + 2];
 #pragma unroll
-    for (int j = 0; j < NPH; ++j) u[j] = cpair(W + C::OFF_BP1 + 2 * j);
+    for (int t = 0; t < NPT; ++t) {
+#pragma unroll
+      for (int j = 0; j < NPH; ++j) u[t][j] = cpair(W + C::OFF_BP1 + 2 * j);
+      float hv[C::DH];
+      load_vec<C::DH>(ns.h + nn[t] * C::HS, hv);
+#pragma unroll
+      for (int i = 0; i < D; ++i) hc[t][i] = hv[i];
+      hc[t][D] = ns.c[nn[t]];
+      hc[t][D + 1] = static_cast<float>(deg[nn[t]]);
+    }
+    mv2n<NPT, D + 2, NPH, C::OFF_WU, C::DP>(W, hc, u);
     {
-      float hc[D + 2];
+      float sv[NPT][2 * D];
 #pragma unroll
-      for (int i = 0; i < D; ++i) hc[i] = hin[i];
-      hc[D] = cn;
-      hc[D + 1] = static_cast<float>(deg[nn]);
-      mv2<D + 2, NPH, C::OFF_WU, C::DP>(W, hc, u);
-      float sv[2 * D];
+      for (int t = 0; t < NPT; ++t)
 #pragma unroll
-      for (int j = 0; j < NP2; ++j) {
-        sv[2 * j] = s[j].x;
-        sv[2 * j + 1] = s[j].y;
+        for (int j = 0; j < NP2; ++j) {
+          sv[t][2 * j] = s[t][j].x;
+          sv[t][2 * j + 1] = s[t][j].y;
+        }
+      mv2n<NPT, 2 * D, NPH, C::OFF_WU + (D + 2) * C::DP, C::DP>(W, sv, u);
+    }
+    float uv[NPT][D];
+    float2 o[NPT][NPH];
+#pragma unroll
+    for (int t = 0; t < NPT; ++t)
+#pragma unroll
+      for (int j = 0; j < NPH; ++j) {
+        const float2 r2 = relu2x(u[t][j]);
+        if (2 * j < D) uv[t][2 * j] = r2.x;
+        if (2 * j + 1 < D) uv[t][2 * j + 1] = r2.y;
+        o[t][j] = cpair(W + C::OFF_BP2 + 2 * j);
       }
-      mv2<2 * D, NPH, C::OFF_WU + (D + 2) * C::DP, C::DP>(W, sv, u);
-    }
-    float uv[D];
-#pragma unroll
-    for (int j = 0; j < NPH; ++j) {
-      const float2 r2 = relu2x(u[j]);
-      if (2 * j < D) uv[2 * j] = r2.x;
-      if (2 * j + 1 < D) uv[2 * j + 1] = r2.y;
-    }
-    float2 o[NPH];
-#pragma unroll
-    for (int j = 0; j < NPH; ++j) o[j] = cpair(W + C::OFF_BP2 + 2 * j);
-    mv2<D, NPH, C::OFF_WP2, C::DP>(W, uv, o);
-    float hn[C::DH];
-    float2 fin = make_float2(0.f, 0.f);
+    mv2n<NPT, D, NPH, C::OFF_WP2, C::DP>(W, uv, o);
     const float2 al = bcast(alpha);
 #pragma unroll
-    for (int j = 0; j < NPH; ++j) {
-      float2 hp = make_float2(hin[2 * j], 2 * j + 1 < D ? hin[2 * j + 1] : 0.f);
-      hp = ffma2(al, o[j], hp);
-      fin = ffma2(hp, make_float2(0.f, 0.f), fin);  // NaN iff some h is non-finite (dss.py:324)
-      hn[2 * j] = hp.x;
-      hn[2 * j + 1] = (2 * j + 1 < D) ? hp.y : 0.f;
+    for (int t = 0; t < NPT; ++t) {
+      const int n = n0 + 32 * t + lane;
+      float hn[C::DH];
+      float2 fin = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < NPH; ++j) {
+        float2 hp = make_float2(hc[t][2 * j], 2 * j + 1 < D ? hc[t][2 * j + 1] : 0.f);
+        hp = ffma2(al, o[t][j], hp);
+        fin = ffma2(hp, make_float2(0.f, 0.f), fin);  // NaN iff some h is non-finite (dss.py:324)
+        hn[2 * j] = hp.x;
+        hn[2 * j + 1] = (2 * j + 1 < D) ? hp.y : 0.f;
+      }
+      if ((fin.x != 0.f || fin.y != 0.f) && first_bad == 0 && n < k) first_bad = layer_no;
+      // every thread of the warp has read its nodes' h above (same iteration), so the
+      // in-place update cannot race; lanes past k write the dummy row k
+      store_vec<C::DH>(ns.h + min(n, k) * C::HS, hn);
     }
-    // lanes past k write the dummy h row k (branch-free, see phase A)
-    if ((fin.x != 0.f || fin.y != 0.f) && first_bad == 0 && n < k) first_bad = layer_no;
-    store_vec<C::DH>(ns.h + min(n, k) * C::HS, hn);
   }
   if (first_bad != 0 && *bad == 0) *bad = first_bad;
   __syncthreads();
@@ -285,7 +346,7 @@ struct GnnShared {
   double scale;
 };
 
-template <int D, int MODE, bool SLOTS>
+template <int D, int MODE, bool SLOTS, int NPT>
 __device__ __forceinline__ void gnn_body(const GnnArgs& a, GnnShared& sh, int sub, int pos0,
                                          int k) {
   using C = Cfg<D>;
@@ -378,7 +439,7 @@ __device__ __forceinline__ void gnn_body(const GnnArgs& a, GnnShared& sh, int su
 #define DDM_LAYER(LL)                                                                        \
   if constexpr (LL < C::LMAX) {                                                              \
     if (LL < a.nl)                                                                           \
-      gnn_layer<D, MODE, LL * C::STRIDE>(0, k, warp, gq, gh, gc, xy, a.edges, so, dg, a.alpha, \
+      gnn_layer<D, MODE, LL * C::STRIDE, NPT>(0, k, warp, gq, gh, gc, xy, a.edges, so, dg, a.alpha, \
                                          &sh_bad, a.layer0 + LL);                            \
   }
       DDM_LAYER(0) DDM_LAYER(1) DDM_LAYER(2) DDM_LAYER(3) DDM_LAYER(4)
@@ -387,7 +448,7 @@ __device__ __forceinline__ void gnn_body(const GnnArgs& a, GnnShared& sh, int su
     } else {
 #pragma unroll 1
       for (int l = 0; l < a.nl; ++l)
-        gnn_layer<D, MODE, -1>(l * C::STRIDE, k, warp, gq, gh, gc, xy, a.edges, so, dg, a.alpha,
+        gnn_layer<D, MODE, -1, NPT>(l * C::STRIDE, k, warp, gq, gh, gc, xy, a.edges, so, dg, a.alpha,
                                &sh_bad, a.layer0 + l);
     }
   }
@@ -438,13 +499,13 @@ __device__ __forceinline__ void gnn_body(const GnnArgs& a, GnnShared& sh, int su
 // Subdomains whose node state (h, Q, c) fits the launch's shared memory (k <=
 // a.cap0): one CTA per subdomain in LPT order, compile-time bank slots.
 template <int D>
-__global__ void __launch_bounds__(kGnnThreads, 1) gnn_kernel(GnnArgs a) {
+__global__ void __launch_bounds__(kGnnThreads / kGnnNpt, 1) gnn_kernel(GnnArgs a) {
   if (a.skip != nullptr && uni(*a.skip) != 0) return;
   __shared__ GnnShared sh;
   const int sub = uni(a.order[a.order_begin + blockIdx.x]);
   const int pos0 = uni(a.sub_ptr[sub]);
   const int k = uni(a.sub_ptr[sub + 1] - pos0);
-  gnn_body<D, 0, true>(a, sh, sub, pos0, k);
+  gnn_body<D, 0, true, kGnnNpt>(a, sh, sub, pos0, k);
 }
 
 // The few oversized subdomains (k > a.cap0): Q alone in shared memory (k <= a.cap1,
@@ -458,9 +519,9 @@ __global__ void __launch_bounds__(kGnnThreads, 1) gnn_big_kernel(GnnArgs a) {
   const int pos0 = uni(a.sub_ptr[sub]);
   const int k = uni(a.sub_ptr[sub + 1] - pos0);
   if (k <= a.cap1) {
-    gnn_body<D, 1, true>(a, sh, sub, pos0, k);
+    gnn_body<D, 1, true, 1>(a, sh, sub, pos0, k);
   } else {
-    gnn_body<D, 2, false>(a, sh, sub, pos0, k);
+    gnn_body<D, 2, false, 1>(a, sh, sub, pos0, k);
   }
 }
 

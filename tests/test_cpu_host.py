@@ -16,7 +16,7 @@ HEADER = os.path.join(ROOT, "include", "ddmgnn_b200.h")
 
 def _declared():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"\b(ddmgnn_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(ddmgnn_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_library_exports_every_declared_symbol():
