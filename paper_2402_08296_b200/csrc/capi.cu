@@ -63,6 +63,14 @@ static void dfree(T*& p) {
   p = nullptr;
 }
 
+template <typename T>
+static cudaError_t upload(T** dst, const std::vector<T>& v) {
+  cudaError_t e = dalloc(dst, std::max<size_t>(v.size(), 1));
+  if (e != cudaSuccess) return e;
+  if (v.empty()) return cudaSuccess;
+  return cudaMemcpy(*dst, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice);
+}
+
 struct ddmgnn_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -73,6 +81,9 @@ struct ddmgnn_ctx {
   long long nnz = 0;
   int *d_rowptr = nullptr, *d_col = nullptr;
   double* d_val = nullptr;
+  int *d_sell_off = nullptr, *d_sell_col = nullptr;  // SELL-32 copy for the SpMV
+  double* d_sell_val = nullptr;
+  SellMatrix sell;
   // inputs kept on the host until build
   std::vector<double> coords;
   std::vector<int64_t> sub_ptr, sub_idx;
@@ -172,6 +183,7 @@ extern "C" void ddmgnn_destroy(ddmgnn_ctx* c) {
   cudaStreamSynchronize(c->stream);
   free_layout(c);
   dfree(c->d_rowptr); dfree(c->d_col); dfree(c->d_val);
+  dfree(c->d_sell_off); dfree(c->d_sell_col); dfree(c->d_sell_val);
   dfree(c->d_bank); dfree(c->d_cinv); dfree(c->d_status);
   dfree(c->d_rin); dfree(c->d_zout);
   dfree(c->d_b); dfree(c->d_u); dfree(c->d_r); dfree(c->d_p); dfree(c->d_q); dfree(c->d_z);
@@ -219,6 +231,35 @@ extern "C" int ddmgnn_set_matrix(ddmgnn_ctx* c, int64_t n, int64_t nnz, const in
   if (nnz) {
     CUDA_TRY(cudaMemcpy(c->d_col, indices, sizeof(int) * nnz, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(c->d_val, data, sizeof(double) * nnz, cudaMemcpyHostToDevice));
+  }
+  {  // SELL-32 copy (slice = 32 rows, width = longest row of the slice)
+    const int slices = static_cast<int>((n + 31) / 32);
+    std::vector<int> off(slices + 1, 0);
+    for (int q = 0; q < slices; ++q) {
+      int64_t w = 0;
+      for (int64_t i = 32ll * q; i < std::min<int64_t>(n, 32ll * q + 32); ++i)
+        w = std::max<int64_t>(w, indptr[i + 1] - indptr[i]);
+      if (off[q] + 32 * w >= (1ll << 31)) return fail(kValueError, "matrix too large for SELL-32");
+      off[q + 1] = off[q] + static_cast<int>(32 * w);
+    }
+    const size_t pad = std::max(off[slices], 1);
+    std::vector<int> sc(pad, -1);
+    std::vector<double> sv(pad, 0.0);
+    for (int64_t i = 0; i < n; ++i) {
+      const int base = off[i >> 5] + static_cast<int>(i & 31);
+      for (int64_t t = indptr[i]; t < indptr[i + 1]; ++t) {
+        sc[base + 32 * (t - indptr[i])] = indices[t];
+        sv[base + 32 * (t - indptr[i])] = data[t];
+      }
+    }
+    CUDA_TRY(upload(&c->d_sell_off, off));
+    CUDA_TRY(upload(&c->d_sell_col, sc));
+    CUDA_TRY(upload(&c->d_sell_val, sv));
+    c->sell.n = static_cast<int>(n);
+    c->sell.slices = slices;
+    c->sell.off = c->d_sell_off;
+    c->sell.col = c->d_sell_col;
+    c->sell.val = c->d_sell_val;
   }
   // Krylov vectors
   CUDA_TRY(dalloc(&c->d_b, n)); CUDA_TRY(dalloc(&c->d_u, n)); CUDA_TRY(dalloc(&c->d_r, n));
@@ -301,13 +342,6 @@ extern "C" int ddmgnn_set_coarse_inverse(ddmgnn_ctx* c, int64_t k, const double*
   return kOk;
 }
 
-template <typename T>
-static cudaError_t upload(T** dst, const std::vector<T>& v) {
-  cudaError_t e = dalloc(dst, std::max<size_t>(v.size(), 1));
-  if (e != cudaSuccess) return e;
-  if (v.empty()) return cudaSuccess;
-  return cudaMemcpy(*dst, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice);
-}
 
 // Plan the shared-memory placement for the current latent dimension and
 // (re)allocate the per-node global scratch it needs.
@@ -606,7 +640,7 @@ extern "C" int ddmgnn_local_outputs(ddmgnn_ctx* c, double** zloc, double** scale
 extern "C" int ddmgnn_spmv(ddmgnn_ctx* c, const double* x, double* y, void* stream) {
   if (!c || !c->n) return fail(kStateError, "no matrix set");
   CUDA_TRY(cudaSetDevice(c->device));
-  CUDA_TRY(launch_spmv(c->n, c->d_rowptr, c->d_col, c->d_val, x, y, pick(c, stream)));
+  CUDA_TRY(launch_spmv(c->sell, x, y, pick(c, stream)));
   return kOk;
 }
 
@@ -616,7 +650,7 @@ extern "C" int ddmgnn_spmv(ddmgnn_ctx* c, const double* x, double* y, void* stre
 static cudaError_t enqueue_iteration(ddmgnn_ctx* c, int level, cudaStream_t s) {
   const int n = c->n;
   int* sw = &c->d_st->status;
-  cudaError_t e = launch_spmv_pq(n, c->d_rowptr, c->d_col, c->d_val, c->d_p, c->d_q,
+  cudaError_t e = launch_spmv_pq(c->sell, c->d_p, c->d_q,
                                  c->d_partials, c->d_st, s);
   if (e != cudaSuccess) return e;
   e = launch_update(n, c->d_u, c->d_r, c->d_p, c->d_q, c->d_partials, c->d_st, c->d_hist,
@@ -673,7 +707,7 @@ static int pcg_prologue(ddmgnn_ctx* c, const double* b, const double* u0, int de
   CUDA_TRY(cudaMemcpyAsync(c->d_b, b, bytes, kin, s));
   if (u0) {
     CUDA_TRY(cudaMemcpyAsync(c->d_u, u0, bytes, kin, s));
-    CUDA_TRY(launch_spmv(n, c->d_rowptr, c->d_col, c->d_val, c->d_u, c->d_q, s));
+    CUDA_TRY(launch_spmv(c->sell, c->d_u, c->d_q, s));
     CUDA_TRY(launch_pcg_init_u0(n, c->d_b, c->d_q, c->d_r, c->d_partials, c->d_st, c->d_hist, s));
   } else {
     CUDA_TRY(cudaMemsetAsync(c->d_u, 0, bytes, s));
@@ -810,7 +844,7 @@ extern "C" int ddmgnn_pcg_host_precond(ddmgnn_ctx* c, const double* b, const dou
                              cudaMemcpyHostToDevice, s));
   }
   for (int it = 0; it < max_iter; ++it) {
-    CUDA_TRY(launch_spmv_pq(n, c->d_rowptr, c->d_col, c->d_val, c->d_p, c->d_q, c->d_partials,
+    CUDA_TRY(launch_spmv_pq(c->sell, c->d_p, c->d_q, c->d_partials,
                             c->d_st, s));
     CUDA_TRY(launch_update(n, c->d_u, c->d_r, c->d_p, c->d_q, c->d_partials, c->d_st, c->d_hist,
                            0, s));

@@ -156,11 +156,17 @@ cudaError_t launch_prolong(int n, int two_level, const int* tptr, const int2* te
                            const double* pou, const double* y, const double* scale,
                            const double* zloc, double* z, const double* r, double* partials,
                            PcgState* st, int mode, const int* skip, cudaStream_t s);
-cudaError_t launch_spmv(int n, const int* rowptr, const int* col, const double* val,
-                        const double* x, double* y, cudaStream_t s);
-cudaError_t launch_spmv_pq(int n, const int* rowptr, const int* col, const double* val,
-                           const double* p, double* q, double* partials, PcgState* st,
-                           cudaStream_t s);
+// SELL-32 copy of A (built in set_matrix): slice q = rows 32q..32q+31, entry
+// (e, lane) at off[q] + 32 e + lane; padding entries have col = -1, val = 0.
+struct SellMatrix {
+  int n = 0, slices = 0;
+  const int* off = nullptr;    // slices + 1
+  const int* col = nullptr;    // padded entries
+  const double* val = nullptr;
+};
+cudaError_t launch_spmv(const SellMatrix& m, const double* x, double* y, cudaStream_t s);
+cudaError_t launch_spmv_pq(const SellMatrix& m, const double* p, double* q, double* partials,
+                           PcgState* st, cudaStream_t s);
 cudaError_t launch_update(int n, double* u, double* r, const double* p, const double* q,
                           double* partials, PcgState* st, double* hist, int identity_precond,
                           cudaStream_t s);

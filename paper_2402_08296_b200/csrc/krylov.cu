@@ -1,7 +1,7 @@
 // Krylov-loop and gluing kernels for sm_100a (all fp64, HBM-bound).
 //
 // Replaces, per PCG iteration of pkg/src/ddmgnn/sparse.py:76-127:
-//   q = A p (:107) + <p, q> (:108) + alpha (:111)          -> spmv_pq_kernel
+//   q = A p (:107) + <p, q> (:108) + alpha (:111)          -> spmv_kernel<true> (SELL-32)
 //   u += alpha p, r -= alpha q (:112-113) + ||r|| (:114)    -> update_kernel
 //   p = z + beta p (:126)                                   -> pupdate_kernel
 // and the two-level gluing of hybrid.py:117,133-135:
@@ -91,42 +91,48 @@ __device__ bool grid_sum(double (&v)[NV], double* partials, unsigned int* ticket
 }
 
 // ------------------------------------------------------------------ SpMV
-// CSR SpMV, one row per thread, the block's nonzeros staged through SMEM with
-// coalesced loads; each row is summed sequentially in column order (scipy
-// csr_matvec order).
+// SELL-32 SpMV (sliced ELL built once from the CSR in set_matrix): thread per row,
+// slice = 32 consecutive rows = one warp, entry (e, lane) of slice q at
+// off[q] + 32 e + lane, so every col/val load of the warp is one coalesced
+// 128 B / 256 B request.  Padding entries have col = -1.  Each row is summed
+// sequentially in ascending column order (scipy csr_matvec order), so y is
+// bit-identical to the reference's A @ x.  Loads are issued four entries ahead
+// of the dependent adds (memory-level parallelism for the HBM-bound stream).
 constexpr int kSpmvRows = 256;
-constexpr int kSpmvStage = 3072;
 
 template <bool PQ>
-__global__ void __launch_bounds__(kSpmvRows) spmv_kernel(int n, const int* __restrict__ rowptr,
-                                                         const int* __restrict__ col,
-                                                         const double* __restrict__ val,
-                                                         const double* __restrict__ x,
+__global__ void __launch_bounds__(kSpmvRows) spmv_kernel(SellMatrix m, const double* __restrict__ x,
                                                          double* __restrict__ y, double* partials,
                                                          PcgState* st) {
   if (PQ && st->status != kRunning) return;
-  __shared__ int s_col[kSpmvStage];
-  __shared__ double s_val[kSpmvStage];
-  const int r0 = blockIdx.x * kSpmvRows;
-  const int r1 = min(n, r0 + kSpmvRows);
-  const int row = r0 + threadIdx.x;
-  const int e0 = rowptr[r0], e1 = rowptr[r1];
-  const bool staged = (e1 - e0) <= kSpmvStage;
-  if (staged) {
-    for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-      s_col[e - e0] = col[e];
-      s_val[e - e0] = val[e];
+  const int row = blockIdx.x * kSpmvRows + threadIdx.x;
+  double pq = 0.0;
+  if (row < m.n) {
+    const int q = row >> 5;
+    const int off = __ldg(&m.off[q]);
+    const int w = (__ldg(&m.off[q + 1]) - off) >> 5;
+    const int* __restrict__ cp = m.col + off + (row & 31);
+    const double* __restrict__ vp = m.val + off + (row & 31);
+    double acc = 0.0;
+    int e = 0;
+    for (; e + 4 <= w; e += 4) {
+      int c[4];
+      double v[4], xv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        c[u] = __ldcs(cp + 32 * (e + u));
+        v[u] = __ldcs(vp + 32 * (e + u));
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) xv[u] = c[u] >= 0 ? __ldg(&x[c[u]]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (c[u] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
     }
-  }
-  __syncthreads();
-  double acc = 0.0, pq = 0.0;
-  if (row < r1) {
-    const int b = rowptr[row], e = rowptr[row + 1];
-    if (staged) {
-      for (int t = b; t < e; ++t)
-        acc = __dadd_rn(acc, __dmul_rn(s_val[t - e0], __ldg(&x[s_col[t - e0]])));
-    } else {
-      for (int t = b; t < e; ++t) acc = __dadd_rn(acc, __dmul_rn(val[t], __ldg(&x[col[t]])));
+    for (; e < w; ++e) {
+      const int c = __ldcs(cp + 32 * e);
+      const double v = __ldcs(vp + 32 * e);
+      if (c >= 0) acc = __dadd_rn(acc, __dmul_rn(v, __ldg(&x[c])));
     }
     y[row] = acc;
     if (PQ) pq = x[row] * acc;
@@ -144,19 +150,17 @@ __global__ void __launch_bounds__(kSpmvRows) spmv_kernel(int n, const int* __res
   }
 }
 
-cudaError_t launch_spmv(int n, const int* rowptr, const int* col, const double* val,
-                        const double* x, double* y, cudaStream_t s) {
-  if (n <= 0) return cudaSuccess;
-  spmv_kernel<false><<<(n + kSpmvRows - 1) / kSpmvRows, kSpmvRows, 0, s>>>(
-      n, rowptr, col, val, x, y, nullptr, nullptr);
+cudaError_t launch_spmv(const SellMatrix& m, const double* x, double* y, cudaStream_t s) {
+  if (m.n <= 0) return cudaSuccess;
+  spmv_kernel<false><<<(m.n + kSpmvRows - 1) / kSpmvRows, kSpmvRows, 0, s>>>(m, x, y, nullptr,
+                                                                           nullptr);
   return cudaGetLastError();
 }
 
-cudaError_t launch_spmv_pq(int n, const int* rowptr, const int* col, const double* val,
-                           const double* p, double* q, double* partials, PcgState* st,
-                           cudaStream_t s) {
-  spmv_kernel<true><<<(n + kSpmvRows - 1) / kSpmvRows, kSpmvRows, 0, s>>>(
-      n, rowptr, col, val, p, q, partials, st);
+cudaError_t launch_spmv_pq(const SellMatrix& m, const double* p, double* q, double* partials,
+                           PcgState* st, cudaStream_t s) {
+  spmv_kernel<true><<<(m.n + kSpmvRows - 1) / kSpmvRows, kSpmvRows, 0, s>>>(m, p, q, partials,
+                                                                          st);
   return cudaGetLastError();
 }
 
