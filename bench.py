@@ -63,9 +63,33 @@ def parse():
 
 
 def gnn_flops(k_bar, d, v, e):
-    """Minimal factorised FP32 flops of one GNN apply."""
+    """SURVEY.md §8d's F_gnn: minimal factorised FP32 flops of one GNN apply."""
     per_node = (8 * d * d + 2 * d) + (4 * d * d + 4 * d) + (2 * (3 * d + 1) * d + 2 * d * d + 2 * d) + 2 * d
     return float(k_bar * (per_node * v + 16 * d * e) + (2 * d * d + 2 * d) * v)
+
+
+def gnn_flops_exec(k_bar, d, v, e):
+    """FP32 flops the fused kernel executes (FMA = 2, relu not counted):
+    per node and layer Q and P ((d+2) -> 2d each), psi first layer ((3d+2) -> d with the
+    messages' second layer folded in), psi second layer (d -> d), h update (d);
+    per edge and layer P+Q add, |d| FMA, sum add over 2d hidden units; decoder once."""
+    dh = (d + 1) // 2 * 2
+    per_node = 2 * (2 * (d + 2) * 2 * d) + 2 * (3 * d + 2) * dh + 2 * d * dh + 2 * dh
+    per_edge = 2 * d * (1 + 2 + 1)
+    return float(k_bar * (per_node * v + per_edge * e) + (2 * d * dh + 2 * d) * v)
+
+
+def profiled_traffic(kernel):
+    """DRAM bytes per launch from this round's committed ncu capture (profiles/)."""
+    import glob
+
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")), reverse=True):
+        try:
+            t = json.load(open(path))[kernel]
+            return t["traffic_bytes"], os.path.relpath(path, ROOT)
+        except (OSError, ValueError, KeyError):
+            continue
+    return None, None
 
 
 class ClockSampler:
@@ -328,14 +352,16 @@ def run_ours(args):
     spmv_ms = sum(e0.elapsed_time(e1) for e0, e1 in sp_ev) / len(sp_ev)
     spmv_bytes = 12 * a.nnz + 20 * n
 
-    # ---- end to end through the C ABI with host buffers ----
-    r_host = np.random.default_rng(rank).standard_normal(n)
+    # ---- end to end through the C ABI with host buffers (pinned, per the contract) ----
+    r_pin = torch.from_numpy(np.random.default_rng(rank).standard_normal(n)).pin_memory()
+    z_pin = torch.empty(n, dtype=torch.float64).pin_memory()
+    r_host, z_host = r_pin.numpy(), z_pin.numpy()
     for _ in range(2):
-        ctx.apply_host(r_host, lvl)
+        ctx.apply_host(r_host, lvl, out=z_host)
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        ctx.apply_host(r_host, lvl)
+        ctx.apply_host(r_host, lvl, out=z_host)
     t_e2e = (time.perf_counter() - t0) / args.steps
     e2e_t = torch.tensor([t_e2e], device=dev)
     if world > 1:
@@ -353,15 +379,25 @@ def run_ours(args):
     except (OSError, ValueError):
         pass
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    hbm_src = "MEASURED_PEAKS.json (of measured)" if "hbm_gbs" in peaks else \
+        "fallback 6.65 TB/s from B200_PROFILING.md (of fallback; MEASURED_PEAKS.json absent)"
+    sm_mhz = peaks.get("sm_max_mhz") or clk.summary().get("sm_max_mhz") or 1965.0
     fp32_peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
-    flops = gnn_flops(info["k_bar"], info["d"], info["V"], info["E"])
+    flops = gnn_flops_exec(info["k_bar"], info["d"], info["V"], info["E"])
+    flops_survey = gnn_flops(info["k_bar"], info["d"], info["V"], info["E"])
     achieved = flops / (gnn_ms * 1e-3) / 1e12
+    gnn_traffic, traffic_src = profiled_traffic("gnn_kernel")
+    spmv_traffic, _ = profiled_traffic("spmv_kernel")
     n_gnn_launches = info["n_chunks"] * (1 + (1 if info["n_big"] else 0))
     per_step_launches = n_gnn_launches + (1 if lvl == 2 else 0) + 1
     clocks = clk.summary()
     if rank == 0:
         cpu = cpu_baseline(prob, args, args.cpu_seconds) if world == 1 else None
+        if cpu is not None and pcg is not None:
+            # the reference PCG's cost is ~all in apply
+            cpu["time_to_solution_s_extrapolated"] = cpu["seconds_per_apply"] * (pcg["iterations"] + 1)
+            cpu["time_to_solution_note"] = ("per-apply CPU time x (GPU iteration count + 1); the "
+                                            "reference's SpMV/BLAS-1 (<1%) not included")
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
@@ -377,18 +413,24 @@ def run_ours(args):
                 "parallelism": f"{world} rank(s); each rank owns a full config-C instance",
             },
             "roofline": {
-                "kernel": "gnn_kernel (fused restriction + 10 message-passing layers + decoder)",
+                "kernel": "gnn_kernel + concurrent gnn_big_kernel (fused restriction + "
+                          f"{info['k_bar']} message-passing layers + decoder)",
                 "bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp32_peak, "traffic": None,
-                "algorithmic": f"F_gnn = k(2120 V + 160 E) + 220 V = {flops:.3e} flop per launch",
-                "peak_source": "148 SM x 128 FP32 lanes x 2 x sm_max_mhz (MEASURED_PEAKS.json); "
-                               "MEASURED_PEAKS has no FP32 CUDA-core figure",
+                "frac": achieved / fp32_peak, "traffic": gnn_traffic,
+                "traffic_source": traffic_src,
+                "algorithmic": f"executed FP32 flops k(1820 V + 80 E) + 220 V (d=10) = {flops:.3e} "
+                               "per launch (DESIGN.md §4)",
+                "survey_F_gnn": flops_survey,
+                "survey_F_gnn_tflops": flops_survey / (gnn_ms * 1e-3) / 1e12,
+                "peak_source": "148 SM x 128 FP32 lanes x 2 flop x sm_max_mhz (FP32 CUDA-core "
+                               "peak; MEASURED_PEAKS has no FP32 figure)",
                 "gnn_ms": gnn_ms, "share_of_step": gnn_ms / ms,
             },
             "roofline_spmv": {
                 "bound": "hbm", "achieved": spmv_bytes / (spmv_ms * 1e-3) / 1e9, "peak": hbm_peak,
                 "unit": "GB/s", "frac": spmv_bytes / (spmv_ms * 1e-3) / 1e9 / hbm_peak,
-                "traffic": None, "ms": spmv_ms, "algorithmic_bytes": spmv_bytes,
+                "traffic": spmv_traffic, "ms": spmv_ms, "algorithmic_bytes": spmv_bytes,
+                "peak_source": hbm_src,
             },
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n,

@@ -195,9 +195,9 @@ class Context:
                                                   vec.ctypes.data_as(_pf)))
         return src[:n], dst[:n], vec[:n]
 
-    def apply_host(self, r: np.ndarray, level: int) -> np.ndarray:
+    def apply_host(self, r: np.ndarray, level: int, out: np.ndarray | None = None) -> np.ndarray:
         r = np.ascontiguousarray(r, dtype=np.float64)
-        z = np.empty_like(r)
+        z = np.empty_like(r) if out is None else out
         check(self._lib.ddmgnn_apply_host(self._h, dptr(r), dptr(z), int(level)))
         return z
 

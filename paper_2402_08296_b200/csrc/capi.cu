@@ -599,14 +599,29 @@ extern "C" int ddmgnn_apply_host(ddmgnn_ctx* c, const double* r, double* z, int 
   CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t s = c->stream;
   const size_t bytes = sizeof(double) * c->n;
-  std::memcpy(c->h_pin_a, r, bytes);
-  CUDA_TRY(cudaMemcpyAsync(c->d_rin, c->h_pin_a, bytes, cudaMemcpyHostToDevice, s));
+  // page-locked caller buffers are DMA'd directly; pageable ones go through the
+  // context's pinned staging buffers
+  auto pinned = [](const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+  };
+  const bool r_pin = pinned(r), z_pin = pinned(z);
+  const double* src = r;
+  if (!r_pin) {
+    std::memcpy(c->h_pin_a, r, bytes);
+    src = c->h_pin_a;
+  }
+  CUDA_TRY(cudaMemcpyAsync(c->d_rin, src, bytes, cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaMemsetAsync(c->d_status, 0, sizeof(int), s));
   CUDA_TRY(enqueue_apply(c, c->d_rin, c->d_zout, level, c->d_status, nullptr, 0, s));
-  CUDA_TRY(cudaMemcpyAsync(c->h_pin_b, c->d_zout, bytes, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaMemcpyAsync(z_pin ? z : c->h_pin_b, c->d_zout, bytes, cudaMemcpyDeviceToHost, s));
   st = check_status_word(c, s);
   if (st) return st;
-  std::memcpy(z, c->h_pin_b, bytes);
+  if (!z_pin) std::memcpy(z, c->h_pin_b, bytes);
   return kOk;
 }
 
