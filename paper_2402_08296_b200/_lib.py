@@ -15,7 +15,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libddmgnn_b200.so")
+# DDMGNN_B200_LIB selects an alternative in-tree build (kernel experiments)
+LIB_PATH = os.environ.get("DDMGNN_B200_LIB") or os.path.join(_HERE, "libddmgnn_b200.so")
 
 PRECOND_NONE = 0
 LEVEL_ONE = 1

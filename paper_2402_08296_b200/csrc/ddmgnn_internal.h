@@ -49,7 +49,10 @@ enum DevStatus : int {
   kPrecondError = 5,
 };
 
-constexpr int kGnnThreads = 768;  // max CTA size (big-subdomain kernel)
+#ifndef GNN_THREADS
+#define GNN_THREADS 768
+#endif
+constexpr int kGnnThreads = GNN_THREADS;  // GNN CTA size (24 warps: 2 slices/warp at k~1450)
 constexpr int kGnnNpt = 1;        // nodes per thread of the main GNN kernel (CTA = 512 / kGnnNpt)
 constexpr int kConstFloats = 16384;  // 64 KB constant bank
 constexpr int kGnnSmemMax = 227 * 1024 - 1024;  // dynamic smem cap (static smem < 1 KB)

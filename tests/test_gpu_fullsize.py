@@ -1,0 +1,80 @@
+"""GPU checks at BASELINE sizes: config B (~100k DOFs) apply
+against the CPU oracle (the oracle finishes one forward in seconds there), and
+size-independent properties at config C (~1M DOFs): exact positive
+homogeneity z(2r) = 2 z(r) (the reference normalises r_i, hybrid.py:103-108, so
+scaling by a power of two is exact end to end), bitwise repeatability, zero in
+-> zero out, and the SpMV against scipy bit for bit (sequential row sums,
+sparse.py:107)."""
+import numpy as np
+import pytest
+
+from conftest import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def ddm():
+    import paper_2402_08296_b200 as m
+
+    return m
+
+
+def _build(target, ns=1000, overlap=2):
+    from paper_2402_08296_b200.problem import ProblemConfig, build_problem
+
+    return build_problem(0, ProblemConfig(target, 0.2, ns, overlap))
+
+
+@pytest.fixture(scope="module")
+def config_b():
+    return _build(100_000)
+
+
+@pytest.fixture(scope="module")
+def config_c():
+    return _build(1_000_000)
+
+
+@pytest.mark.parametrize("level", ["one", "two"])
+def test_config_b_apply_matches_oracle(ddm, config_b, level):
+    from oracle import ddm_oracle as orc
+
+    prob = config_b
+    model = ddm.init_model(10, 10, seed=1)
+    p = ddm.build_ddm_gnn(prob.system.a, prob.coords, prob.dec, model, level=level)
+    om = orc.model_from_flat(10, 10, model.alpha, 1, ddm.flat_params(model))
+    ref = orc.OraclePreconditioner(prob.system.a, prob.coords, prob.dec.subdomains, om, level=level)
+    r = np.random.default_rng(0).standard_normal(prob.system.n)
+    assert rel_l2(p(r), ref(r)) < TOL
+
+
+def test_config_c_properties(ddm, config_c):
+    import torch
+
+    prob = config_c
+    p = ddm.build_ddm_gnn(prob.system.a, prob.coords, prob.dec, ddm.init_model(10, 10, seed=1))
+    r = torch.tensor(np.random.default_rng(0).standard_normal(prob.system.n), device="cuda")
+    z1 = p(r)
+    z2 = p(r)
+    assert torch.equal(z1, z2)                       # deterministic
+    assert torch.equal(p(2.0 * r), 2.0 * z1)         # exact positive homogeneity
+    assert torch.count_nonzero(p(torch.zeros_like(r))) == 0
+    assert bool(torch.isfinite(z1).all())
+
+
+def test_config_c_spmv_bitwise(ddm, config_c):
+    import torch
+
+    prob = config_c
+    a = prob.system.a
+    p = ddm.build_ddm_gnn(a, prob.coords, prob.dec, ddm.init_model(2, 10, seed=1), level="one")
+    x = np.random.default_rng(3).standard_normal(a.shape[0])
+    xd = torch.tensor(x, device="cuda")
+    yd = torch.empty_like(xd)
+    st = torch.cuda.current_stream().cuda_stream or 1
+    p.context.spmv_device(xd.data_ptr(), yd.data_ptr(), st)
+    torch.cuda.synchronize()
+    assert np.array_equal(yd.cpu().numpy(), a @ x)
