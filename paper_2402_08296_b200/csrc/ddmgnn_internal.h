@@ -50,9 +50,9 @@ enum DevStatus : int {
 };
 
 #ifndef GNN_THREADS
-#define GNN_THREADS 768
+#define GNN_THREADS 896
 #endif
-constexpr int kGnnThreads = GNN_THREADS;  // GNN CTA size (24 warps: 2 slices/warp at k~1450)
+constexpr int kGnnThreads = GNN_THREADS;  // GNN CTA size (28 warps/SM; measured best of 640-1024)
 constexpr int kGnnNpt = 1;        // nodes per thread of the main GNN kernel (CTA = 512 / kGnnNpt)
 constexpr int kConstFloats = 16384;  // 64 KB constant bank
 constexpr int kGnnSmemMax = 227 * 1024 - 1024;  // dynamic smem cap (static smem < 1 KB)

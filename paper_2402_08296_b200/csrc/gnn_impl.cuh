@@ -296,7 +296,6 @@ __device__ __forceinline__ void gnn_layer(int w_rt, int k, int warp, float* gq, 
           sv[t][2 * j] = s[t][j].x;
           sv[t][2 * j + 1] = s[t][j].y;
         }
-#ifdef GNN_SPLIT_ACC
       // second, independent accumulator chain for the message part (ILP)
       float2 u2[NPT][NPH];
 #pragma unroll
@@ -308,9 +307,6 @@ __device__ __forceinline__ void gnn_layer(int w_rt, int k, int warp, float* gq, 
       for (int t = 0; t < NPT; ++t)
 #pragma unroll
         for (int j = 0; j < NPH; ++j) u[t][j] = fadd2(u[t][j], u2[t][j]);
-#else
-      mv2n<NPT, 2 * D, NPH, C::OFF_WU + (D + 2) * C::DP, C::DP>(W, sv, u);
-#endif
     }
     float uv[NPT][D];
     float2 o[NPT][NPH];

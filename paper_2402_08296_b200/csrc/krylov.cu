@@ -96,7 +96,7 @@ __device__ bool grid_sum(double (&v)[NV], double* partials, unsigned int* ticket
 // off[q] + 32 e + lane, so every col/val load of the warp is one coalesced
 // 128 B / 256 B request.  Padding entries have col = -1.  Each row is summed
 // sequentially in ascending column order (scipy csr_matvec order), so y is
-// bit-identical to the reference's A @ x.  Loads are issued four entries ahead
+// bit-identical to the reference's A @ x.  Loads are issued eight entries ahead
 // of the dependent adds (memory-level parallelism for the HBM-bound stream).
 constexpr int kSpmvRows = 256;
 
@@ -114,25 +114,23 @@ __global__ void __launch_bounds__(kSpmvRows) spmv_kernel(SellMatrix m, const dou
     const int* __restrict__ cp = m.col + off + (row & 31);
     const double* __restrict__ vp = m.val + off + (row & 31);
     double acc = 0.0;
-    int e = 0;
-    for (; e + 4 <= w; e += 4) {
-      int c[4];
-      double v[4], xv[4];
+    // FEM rows are short (7 entries at config C): issue up to 8 col/val loads, then
+    // all their x gathers, then the ordered sum — two dependent memory round trips
+    // per 8 entries instead of one per entry.
+    for (int e0 = 0; e0 < w; e0 += 8) {
+      int c[8];
+      double v[8], xv[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        c[u] = __ldcs(cp + 32 * (e + u));
-        v[u] = __ldcs(vp + 32 * (e + u));
+      for (int u = 0; u < 8; ++u) {
+        const bool in = e0 + u < w;
+        c[u] = in ? __ldcs(cp + 32 * (e0 + u)) : -1;
+        v[u] = in ? __ldcs(vp + 32 * (e0 + u)) : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) xv[u] = c[u] >= 0 ? __ldg(&x[c[u]]) : 0.0;
+      for (int u = 0; u < 8; ++u) xv[u] = c[u] >= 0 ? __ldg(&x[c[u]]) : 0.0;
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < 8; ++u)
         if (c[u] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
-    }
-    for (; e < w; ++e) {
-      const int c = __ldcs(cp + 32 * e);
-      const double v = __ldcs(vp + 32 * e);
-      if (c >= 0) acc = __dadd_rn(acc, __dmul_rn(v, __ldg(&x[c])));
     }
     y[row] = acc;
     if (PQ) pq = x[row] * acc;
@@ -319,27 +317,49 @@ cudaError_t launch_copy(int n, const double* src, double* dst, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ coarse level
-// y = inv(R0 A R0^T) x, warp per row (fp64, row-major inverse).  Replaces the
-// dense LU solve of sparse.py:163 (coarse matrix factorised at setup).
+// y = inv(R0 A R0^T) x (fp64, row-major inverse), 128 threads (4 warps) per row and
+// two rows per block so ~K/2 blocks keep enough loads in flight for the 8 K^2
+// byte stream (a warp per row left it latency bound).  Fixed reduction order.
+// Replaces the dense LU solve of sparse.py:163 (coarse matrix factorised at setup).
+constexpr int kGemvRowThreads = 128;
 __global__ void __launch_bounds__(256) coarse_gemv_kernel(int K, const double* __restrict__ inv,
                                                           const double* __restrict__ x,
                                                           double* __restrict__ y,
                                                           const int* skip) {
   if (skip != nullptr && *skip != kRunning) return;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= K) return;
-  const double* row = inv + static_cast<size_t>(warp) * K;
+  __shared__ double part[2][kGemvRowThreads / 32];
+  const int half = threadIdx.x / kGemvRowThreads;  // which of the block's two rows
+  const int t = threadIdx.x % kGemvRowThreads;
+  const int row = blockIdx.x * 2 + half;
   double acc = 0.0;
-  for (int j = lane; j < K; j += 32) acc = fma(__ldg(&row[j]), __ldg(&x[j]), acc);
+  if (row < K) {
+    const double* rp = inv + static_cast<size_t>(row) * K;
+    int j = t;
+    for (; j + 3 * kGemvRowThreads < K; j += 4 * kGemvRowThreads) {
+      const double a0 = __ldcs(&rp[j]), a1 = __ldcs(&rp[j + kGemvRowThreads]);
+      const double a2 = __ldcs(&rp[j + 2 * kGemvRowThreads]);
+      const double a3 = __ldcs(&rp[j + 3 * kGemvRowThreads]);
+      acc = fma(a0, __ldg(&x[j]), acc);
+      acc = fma(a1, __ldg(&x[j + kGemvRowThreads]), acc);
+      acc = fma(a2, __ldg(&x[j + 2 * kGemvRowThreads]), acc);
+      acc = fma(a3, __ldg(&x[j + 3 * kGemvRowThreads]), acc);
+    }
+    for (; j < K; j += kGemvRowThreads) acc = fma(__ldcs(&rp[j]), __ldg(&x[j]), acc);
+  }
   acc = warp_sum_d(acc);
-  if (lane == 0) y[warp] = acc;
+  if ((threadIdx.x & 31) == 0) part[half][t >> 5] = acc;
+  __syncthreads();
+  if (t == 0 && row < K) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kGemvRowThreads / 32; ++w) s += part[half][w];
+    y[row] = s;
+  }
 }
 
 cudaError_t launch_coarse_gemv(int K, const double* inv, const double* x, double* y,
                                const int* skip, cudaStream_t s) {
-  const int blocks = (K * 32 + 255) / 256;
-  coarse_gemv_kernel<<<blocks, 256, 0, s>>>(K, inv, x, y, skip);
+  coarse_gemv_kernel<<<(K + 1) / 2, 2 * kGemvRowThreads, 0, s>>>(K, inv, x, y, skip);
   return cudaGetLastError();
 }
 
