@@ -105,6 +105,8 @@ struct ddmgnn_ctx {
   // apply scratch
   double *d_r0r = nullptr, *d_scale = nullptr, *d_zloc = nullptr, *d_y = nullptr;
   float *d_hbuf = nullptr, *d_cbuf = nullptr, *d_qbuf = nullptr;
+  int2* d_bslices = nullptr;  // flat path: (subdomain, slice) of the oversized subdomains
+  int n_bslices = 0;
   int *d_bad = nullptr, *d_outbad = nullptr, *d_status = nullptr;
   double *d_rin = nullptr, *d_zout = nullptr;  // host-pointer apply staging
   // pcg
@@ -172,7 +174,8 @@ static void free_layout(ddmgnn_ctx* c) {
   dfree(L.deg); dfree(L.edges); dfree(L.xy); dfree(L.tptr); dfree(L.tent); dfree(L.pou);
   dfree(c->d_r0r); dfree(c->d_scale); dfree(c->d_zloc); dfree(c->d_y);
   dfree(c->d_bad); dfree(c->d_outbad);
-  dfree(c->d_hbuf); dfree(c->d_cbuf); dfree(c->d_qbuf);
+  dfree(c->d_hbuf); dfree(c->d_cbuf); dfree(c->d_qbuf); dfree(c->d_bslices);
+  c->n_bslices = 0;
   c->built = false;
   free_graphs(c);
 }
@@ -350,20 +353,28 @@ static int refresh_classes(ddmgnn_ctx* c) {
   const int d = c->model.d;
   c->gnn_smem = gnn_plan_smem(d, c->lay.k_max, &c->cap0, &c->cap1);
   const auto& sp = c->lay.h_sub_ptr;
-  int nb = 0, n2 = 0;
-  for (int i = 0; i < c->K; ++i) {
+  // oversized subdomains (k > cap0) lead the LPT order; they take the flat path
+  int nb = 0;
+  std::vector<int2> bsl;
+  for (int t = 0; t < c->K; ++t) {
+    const int i = c->lay.h_order[t];
     const int k = sp[i + 1] - sp[i];
-    nb += k > c->cap0;
-    n2 += k > c->cap1;
+    if (k <= c->cap0) break;
+    ++nb;
+    for (int q = 0; q * 32 < k; ++q) bsl.push_back(make_int2(i, q));
   }
   c->n_big = nb;
   const int hs = (d % 2 == 0) ? d : d + 1;
   const int qs = (2 * d + 3) / 4 * 4;
   const size_t V = c->lay.V;
   const bool multi = c->model.n_chunks() > 1;
-  CUDA_TRY(dalloc(&c->d_hbuf, (multi || nb) ? (V + c->K) * hs : 0));  // + dummy row per subdomain
+  // + one dummy row per subdomain (lanes past k / SELL padding targets)
+  CUDA_TRY(dalloc(&c->d_hbuf, (multi || nb) ? (V + c->K) * hs : 0));
   CUDA_TRY(dalloc(&c->d_cbuf, (multi || nb) ? V : 0));
-  CUDA_TRY(dalloc(&c->d_qbuf, n2 ? (V + c->K) * qs : 0));  // + one dummy row per subdomain
+  CUDA_TRY(dalloc(&c->d_qbuf, nb ? (V + c->K) * qs : 0));
+  dfree(c->d_bslices);
+  c->n_bslices = static_cast<int>(bsl.size());
+  if (!bsl.empty()) CUDA_TRY(upload(&c->d_bslices, bsl));
   return kOk;
 }
 
@@ -488,6 +499,7 @@ static cudaError_t enqueue_gnn(ddmgnn_ctx* c, const double* r, int* status, cons
   a.slice_off = L.slice_off; a.deg = L.deg; a.edges = L.edges; a.xy = L.xy; a.pou = L.pou;
   a.r = r; a.r0r = c->d_r0r; a.scale = c->d_scale; a.zloc = c->d_zloc;
   a.hbuf = c->d_hbuf; a.cbuf = c->d_cbuf; a.qbuf = c->d_qbuf;
+  a.bslices = c->d_bslices; a.n_bslices = c->n_bslices;
   a.bad_layer = c->d_bad; a.out_bad = c->d_outbad; a.status = status; a.skip = skip;
   a.alpha = M.alpha;
   const int nch = M.n_chunks();
@@ -504,8 +516,8 @@ static cudaError_t enqueue_gnn(ddmgnn_ctx* c, const double* r, int* status, cons
     const int k_small = c->n_big < c->K ? c->lay.h_sub_ptr[c->lay.h_order[c->n_big] + 1] -
                                               c->lay.h_sub_ptr[c->lay.h_order[c->n_big]]
                                         : 0;
-    e = launch_gnn(M.d, c->K, c->n_big, c->lay.k_max, k_small, c->gnn_smem, a, s, c->side,
-                   c->ev_fork, c->ev_join);
+    e = launch_gnn(M.d, c->K, c->n_big, k_small, c->gnn_smem, a, s, c->side, c->ev_fork,
+                   c->ev_join);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

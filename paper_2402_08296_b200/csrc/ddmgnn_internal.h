@@ -53,7 +53,6 @@ enum DevStatus : int {
 #define GNN_THREADS 896
 #endif
 constexpr int kGnnThreads = GNN_THREADS;  // GNN CTA size (28 warps/SM; measured best of 640-1024)
-constexpr int kGnnNpt = 1;        // nodes per thread of the main GNN kernel (CTA = 512 / kGnnNpt)
 constexpr int kConstFloats = 16384;  // 64 KB constant bank
 constexpr int kGnnSmemMax = 227 * 1024 - 1024;  // dynamic smem cap (static smem < 1 KB)
 
@@ -131,6 +130,8 @@ struct GnnArgs {
   int first, last;   // chunk flags
   int order_begin;   // CTA b handles subdomain order[order_begin + b]
   int cap0, cap1;    // per-CTA node-state placement thresholds (gnn_plan_smem)
+  const int2* bslices;  // flat path: (subdomain, slice) of every slice of a big subdomain
+  int n_bslices;
 };
 int gnn_smem_max_nodes(int d);
 // WQ WP B1 WL WU BP1 WP2 BP2 STRIDE D2P DP DEC_W1 DEC_B1 DEC_W2 DEC_B2 LMAX (gnn_cfg.h)
@@ -138,7 +139,7 @@ int gnn_bank_offsets(int d, int* o);
 cudaError_t gnn_configure_device();
 cudaError_t upload_bank(int d, const float* dev_bank, cudaStream_t s);  // D2D into the constant bank
 size_t gnn_plan_smem(int d, int k_max, int* cap0, int* cap1);
-cudaError_t launch_gnn(int d, int n_ctas, int n_big, int k_max, int k_max_small, size_t smem,
+cudaError_t launch_gnn(int d, int n_ctas, int n_big, int k_max_small, size_t smem,
                        const GnnArgs& a, cudaStream_t s, cudaStream_t side, cudaEvent_t fork,
                        cudaEvent_t join);
 

@@ -118,9 +118,10 @@ size_t gnn_plan_smem(int d, int k_max, int* cap0, int* cap1) {
 }
 
 // Launch the GNN over all subdomains of `order` (LPT, descending size): the first
-// n_big (k > cap0) run in gnn_big_kernel on the side stream `side`, concurrently
-// with gnn_kernel over the rest on `s` (fork/join by events, graph-capturable).
-cudaError_t launch_gnn(int d, int n_ctas, int n_big, int k_max, int k_max_small, size_t smem,
+// n_big (k > cap0) go through the flat node-parallel path on the side stream
+// `side`, concurrently with gnn_kernel over the rest on `s` (fork/join by events,
+// graph-capturable).
+cudaError_t launch_gnn(int d, int n_ctas, int n_big, int k_max_small, size_t smem,
                        const GnnArgs& a, cudaStream_t s, cudaStream_t side, cudaEvent_t fork,
                        cudaEvent_t join) {
   if (n_ctas <= 0) return cudaSuccess;
@@ -128,10 +129,8 @@ cudaError_t launch_gnn(int d, int n_ctas, int n_big, int k_max, int k_max_small,
   if (n_big > 0) {
     if ((e = cudaEventRecord(fork, s)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(side, fork, 0)) != cudaSuccess) return e;
-    GnnArgs b = a;
-    b.order_begin = a.order_begin;
     switch (d) {
-#define X(DD) case DD: e = gnn_launch_big_d##DD(n_big, k_max, smem, b, side); break;
+#define X(DD) case DD: e = gnn_launch_big_d##DD(n_big, 0, 0, a, side); break;
       DDM_GNN_DIMS(X)
 #undef X
       default: return cudaErrorInvalidValue;

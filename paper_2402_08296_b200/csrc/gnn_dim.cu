@@ -1,6 +1,6 @@
 // One latent dimension of the fused GNN kernels per translation unit (compiled
-// with -DGNN_D=<d>; -DGNN_BIG selects the oversized-subdomain kernel): each unit
-// owns its own 64 KB constant bank, and the units compile in parallel.
+// with -DGNN_D=<d>; -DGNN_BIG selects the flat path for oversized subdomains):
+// each unit owns its own 64 KB constant bank, and the units compile in parallel.
 #include "ddmgnn_internal.h"
 
 #ifndef GNN_D
@@ -16,39 +16,73 @@ static __constant__ float c_w[kConstFloats];
 #define DDM_CAT2(a, b) a##b
 #define DDM_CAT(a, b) DDM_CAT2(a, b)
 #ifdef GNN_BIG
-#define DDM_KERNEL gnn_big_kernel
 #define DDM_NAME(x) DDM_CAT(DDM_CAT(x, _big_d), GNN_D)
 #else
-#define DDM_KERNEL gnn_kernel
 #define DDM_NAME(x) DDM_CAT(DDM_CAT(x, _d), GNN_D)
 #endif
 
 namespace ddmgnn {
-
-cudaError_t DDM_NAME(gnn_configure)() {
-  return cudaFuncSetAttribute(DDM_KERNEL<GNN_D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              kGnnSmemMax);
-}
 
 cudaError_t DDM_NAME(gnn_upload)(const float* dev_bank, cudaStream_t s) {
   return cudaMemcpyToSymbolAsync(c_w, dev_bank, sizeof(float) * kConstFloats, 0,
                                  cudaMemcpyDeviceToDevice, s);
 }
 
-// One launch over n_ctas subdomains (order[a.order_begin ...]); k_max = largest
-// subdomain of the launch, smem = dynamic shared memory chosen by the host.
+#ifndef GNN_BIG
+
+cudaError_t DDM_NAME(gnn_configure)() {
+  return cudaFuncSetAttribute(gnn_kernel<GNN_D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              kGnnSmemMax);
+}
+
+// One CTA per subdomain over n_ctas subdomains (order[a.order_begin ...]); k_max =
+// largest subdomain of the launch, smem = dynamic shared memory chosen by the host.
 cudaError_t DDM_NAME(gnn_launch)(int n_ctas, int k_max, size_t smem, const GnnArgs& a,
                                  cudaStream_t s) {
-#ifdef GNN_BIG
-  const int cap = kGnnThreads, npt = 1;
-#else
-  const int cap = kGnnThreads / kGnnNpt, npt = kGnnNpt;
-#endif
-  int threads = ((k_max + 32 * npt - 1) / (32 * npt)) * 32;
-  if (threads > cap) threads = cap;
+  int threads = ((k_max + 31) / 32) * 32;
+  if (threads > kGnnThreads) threads = kGnnThreads;
   if (threads < 64) threads = 64;
-  DDM_KERNEL<GNN_D><<<n_ctas, threads, smem, s>>>(a);
+  gnn_kernel<GNN_D><<<n_ctas, threads, smem, s>>>(a);
   return cudaGetLastError();
 }
+
+#else
+
+cudaError_t DDM_NAME(gnn_configure)() { return cudaSuccess; }
+
+namespace {
+using QFn = void (*)(GnnArgs);
+using UFn = void (*)(GnnArgs, int, int);
+template <int L>
+constexpr QFn qfn() {
+  if constexpr (L < Cfg<GNN_D>::LMAX) return gnn_flat_q<GNN_D, L * Cfg<GNN_D>::STRIDE>;
+  else return nullptr;
+}
+template <int L>
+constexpr UFn ufn() {
+  if constexpr (L < Cfg<GNN_D>::LMAX) return gnn_flat_u<GNN_D, L * Cfg<GNN_D>::STRIDE>;
+  else return nullptr;
+}
+}  // namespace
+
+// Flat path over the n_subs oversized subdomains order[a.order_begin ...]:
+// restriction (first chunk), then per layer of the chunk one launch per phase over
+// all a.n_bslices slices.
+cudaError_t DDM_NAME(gnn_launch)(int n_subs, int /*k_max*/, size_t /*smem*/, const GnnArgs& a,
+                                 cudaStream_t s) {
+  static const QFn qk[10] = {qfn<0>(), qfn<1>(), qfn<2>(), qfn<3>(), qfn<4>(),
+                             qfn<5>(), qfn<6>(), qfn<7>(), qfn<8>(), qfn<9>()};
+  static const UFn uk[10] = {ufn<0>(), ufn<1>(), ufn<2>(), ufn<3>(), ufn<4>(),
+                             ufn<5>(), ufn<6>(), ufn<7>(), ufn<8>(), ufn<9>()};
+  if (n_subs <= 0 || a.n_bslices <= 0) return cudaSuccess;
+  if (a.first) gnn_flat_prologue<GNN_D><<<n_subs, kGnnThreads, 0, s>>>(a);
+  for (int l = 0; l < a.nl; ++l) {
+    qk[l]<<<a.n_bslices, 32, 0, s>>>(a);
+    uk[l]<<<a.n_bslices, 32, 0, s>>>(a, a.layer0 + l, a.last && l == a.nl - 1);
+  }
+  return cudaGetLastError();
+}
+
+#endif
 
 }  // namespace ddmgnn

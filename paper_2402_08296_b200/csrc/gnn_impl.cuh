@@ -105,21 +105,6 @@ __device__ __forceinline__ void mv2(int base, const float (&x)[NIN], float2 (&ac
   }
 }
 
-// The same for NPT nodes at once: every weight pair (one LDCU) feeds NPT FFMA2.
-template <int NPT, int NIN, int NPO, int OFF, int RS>
-__device__ __forceinline__ void mv2n(int base, const float (&x)[NPT][NIN],
-                                     float2 (&acc)[NPT][NPO]) {
-#pragma unroll
-  for (int m = 0; m < NIN; ++m) {
-#pragma unroll
-    for (int j = 0; j < NPO; ++j) {
-      const float2 w = cpair(base + OFF + m * RS + 2 * j);
-#pragma unroll
-      for (int t = 0; t < NPT; ++t) acc[t][j] = ffma2(bcast(x[t][m]), w, acc[t][j]);
-    }
-  }
-}
-
 // [h (D), x, y] of a node: h from the node state, (x, y) subdomain-centred coordinates.
 template <int D>
 __device__ __forceinline__ void load_hxy(const float* hrow, float2 xy, float (&v)[D + 2]) {
@@ -132,213 +117,188 @@ __device__ __forceinline__ void load_hxy(const float* hrow, float2 xy, float (&v
   v[D + 1] = xy.y;
 }
 
-// Per-CTA views of the node state.  MODE 0: h, Q, c in shared memory; MODE 1: Q in
-// shared memory, h and c in per-node global scratch; MODE 2: everything in global
-// scratch (L1/L2 resident).  The mode is chosen per CTA from the subdomain size, so
-// one launch covers every subdomain.
-template <int D, int MODE>
-struct NodeState {
-  float* h;  // k rows of HS floats
-  float* q;  // k rows of QS floats
-  float* c;  // k floats
-  __device__ __forceinline__ NodeState(int k, float* gq, float* gh, float* gc) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    if constexpr (MODE == 0) {
-      q = reinterpret_cast<float*>(smem_raw);
-      h = q + static_cast<size_t>(k + 1) * Cfg<D>::QS;  // Q rows 0..k (k = dummy)
-      c = h + static_cast<size_t>(k + 1) * Cfg<D>::HS;  // h rows 0..k (k = dummy)
-    } else if constexpr (MODE == 1) {
-      q = reinterpret_cast<float*>(smem_raw);
-      h = gh;
-      c = gc;
-    } else {
-      q = gq;
-      h = gh;
-      c = gc;
+// Warp-uniform value (lane 0's): keeps loop bounds and branch conditions that ptxas
+// cannot prove uniform out of divergent control flow (which would demote the
+// weight loads from uniform LDCU to per-thread LDC).
+__device__ __forceinline__ int uni(int v) { return __shfl_sync(0xffffffffu, v, 0); }
+
+// ---------------------------------------------------------------------------- one slice
+// The per-node work of one layer on one SELL slice (32 consecutive local nodes =
+// one warp; node n0 + lane).  `W` is the layer's slot offset in the constant bank:
+// a compile-time constant in every caller, so each weight pair is an
+// immediate-addressed LDCU.128 operand of FFMA2.  No divergent branch: lanes past
+// k recompute node k-1 (phase A, identical store) or write the dummy h row k
+// (phase B), and the edge loop's trip count is the slice width (warp-uniform)
+// with padding records pointing at the dummy Q row k (all -1e30, whose 2 relu term
+// is exactly 0) — that is what keeps the weight loads in uniform registers.
+
+// phase A: destination projection Q_t = [h_t, x_t, y_t] . WQ
+template <int D, int W>
+__device__ __forceinline__ void slice_q(int n0, int k, const float* h, float* q,
+                                        const float2* __restrict__ xy) {
+  using C = Cfg<D>;
+  constexpr int NP2 = C::NP2;
+  const int nn = min(n0 + static_cast<int>(threadIdx.x & 31), k - 1);
+  float hin[D + 2];
+  load_hxy<D>(h + nn * C::HS, __ldg(xy + nn), hin);
+  float2 qa[NP2];
+#pragma unroll
+  for (int j = 0; j < NP2; ++j) qa[j] = make_float2(0.f, 0.f);
+  mv2<D + 2, NP2, W + C::OFF_WQ, C::D2P>(0, hin, qa);
+  float qs[C::QS];
+#pragma unroll
+  for (int j = 0; j < C::QS; ++j) qs[j] = 0.f;
+#pragma unroll
+  for (int j = 0; j < NP2; ++j) {
+    qs[2 * j] = qa[j].x;
+    qs[2 * j + 1] = qa[j].y;
+  }
+  store_vec<C::QS>(q + nn * C::QS, qs);
+}
+
+// phase B: edge aggregation + node update; returns whether the lane's node became
+// non-finite and leaves the updated latent in hn (for a fused decoder)
+template <int D, int W>
+__device__ __forceinline__ bool slice_u(int n0, int k, float* h, const float* q,
+                                        const float* c, const float2* __restrict__ xy,
+                                        const float2* __restrict__ edges, int so, int width,
+                                        const uint16_t* __restrict__ deg, float alpha,
+                                        float (&hn)[Cfg<D>::DH]) {
+  using C = Cfg<D>;
+  constexpr int NP2 = C::NP2, NPH = C::NPH;
+  const int lane = threadIdx.x & 31;
+  const int n = n0 + lane;
+  const int nn = min(n, k - 1);
+  float2 p[NP2], s[NP2];
+  {
+    float hin[D + 2];
+    load_hxy<D>(h + nn * C::HS, __ldg(xy + nn), hin);
+#pragma unroll
+    for (int j = 0; j < NP2; ++j) {
+      p[j] = cpair(W + C::OFF_B1 + 2 * j);
+      s[j] = make_float2(0.f, 0.f);
     }
+    mv2<D + 2, NP2, W + C::OFF_WP, C::D2P>(0, hin, p);
+  }
+  const float2 dummy = make_float2(0.f, __int_as_float(k));
+  const float2* ep = edges + so + lane;
+  float2 rec = width > 0 ? __ldg(ep) : dummy;
+  for (int e = 0; e < width; ++e) {
+    const float2 cur = rec;
+    rec = e + 1 < width ? __ldg(ep + 32 * (e + 1)) : dummy;
+    float qt[C::QS];
+    load_vec<C::QS>(q + __float_as_int(cur.y) * C::QS, qt);
+    const float2 len = bcast(cur.x);
+#pragma unroll
+    for (int j = 0; j < NP2; ++j) {
+      float2 x = fadd2(p[j], make_float2(qt[2 * j], qt[2 * j + 1]));
+      x = ffma2(len, cpair(W + C::OFF_WL + 2 * j), x);
+      s[j] = fadd2(s[j], relu2x(x));
+    }
+  }
+  // psi first layer with the messages' second layer folded in; the message part
+  // accumulates in a second, independent chain (ILP)
+  float2 u[NPH], u2[NPH];
+  float hc[D + 2];
+  {
+    float hv[C::DH];
+    load_vec<C::DH>(h + nn * C::HS, hv);
+#pragma unroll
+    for (int i = 0; i < D; ++i) hc[i] = hv[i];
+    hc[D] = c[nn];
+    hc[D + 1] = static_cast<float>(deg[nn]);
+  }
+#pragma unroll
+  for (int j = 0; j < NPH; ++j) {
+    u[j] = cpair(W + C::OFF_BP1 + 2 * j);
+    u2[j] = make_float2(0.f, 0.f);
+  }
+  mv2<D + 2, NPH, W + C::OFF_WU, C::DP>(0, hc, u);
+  {
+    float sv[2 * D];
+#pragma unroll
+    for (int j = 0; j < NP2; ++j) {
+      sv[2 * j] = s[j].x;
+      sv[2 * j + 1] = s[j].y;
+    }
+    mv2<2 * D, NPH, W + C::OFF_WU + (D + 2) * C::DP, C::DP>(0, sv, u2);
+  }
+  float uv[D];
+  float2 o[NPH];
+#pragma unroll
+  for (int j = 0; j < NPH; ++j) {
+    const float2 r2 = relu2x(fadd2(u[j], u2[j]));
+    if (2 * j < D) uv[2 * j] = r2.x;
+    if (2 * j + 1 < D) uv[2 * j + 1] = r2.y;
+    o[j] = cpair(W + C::OFF_BP2 + 2 * j);
+  }
+  mv2<D, NPH, W + C::OFF_WP2, C::DP>(0, uv, o);
+  const float2 al = bcast(alpha);
+  float2 fin = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int j = 0; j < NPH; ++j) {
+    float2 hp = make_float2(hc[2 * j], 2 * j + 1 < D ? hc[2 * j + 1] : 0.f);
+    hp = ffma2(al, o[j], hp);
+    fin = ffma2(hp, make_float2(0.f, 0.f), fin);  // NaN iff some h is non-finite (dss.py:324)
+    hn[2 * j] = hp.x;
+    hn[2 * j + 1] = (2 * j + 1 < D) ? hp.y : 0.f;
+  }
+  // the lane's own row only (nobody else reads h): in-place update; lanes past k
+  // write the dummy row k
+  store_vec<C::DH>(h + min(n, k) * C::HS, hn);
+  return (fin.x != 0.f || fin.y != 0.f) && n < k;
+}
+
+// decoder of the final layer (dss.py:327) on one latent (immediate offsets)
+template <int D>
+__device__ __forceinline__ float decode(const float (&hv)[Cfg<D>::DH]) {
+  using C = Cfg<D>;
+  float hd[D];
+#pragma unroll
+  for (int i = 0; i < D; ++i) hd[i] = hv[i];
+  float2 u[C::NPH];
+#pragma unroll
+  for (int j = 0; j < C::NPH; ++j) u[j] = cpair(C::DEC_B1 + 2 * j);
+  mv2<D, C::NPH, C::DEC_W1, C::DP>(0, hd, u);
+  float o = c_w[C::DEC_B2];
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    const float ui = (i & 1) ? u[i >> 1].y : u[i >> 1].x;
+    o = fmaf(relu_nan(ui), c_w[C::DEC_W2 + i], o);
+  }
+  return o;
+}
+
+// ---------------------------------------------------------------------------- CTA path
+// Node state (h, Q, c) of the CTA's subdomain in shared memory: Q rows 0..k
+// (k = dummy), h rows 0..k (k = dummy), c.
+template <int D>
+struct SmemState {
+  float *q, *h, *c;
+  __device__ __forceinline__ explicit SmemState(int k) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    q = reinterpret_cast<float*>(smem_raw);
+    h = q + static_cast<size_t>(k + 1) * Cfg<D>::QS;
+    c = h + static_cast<size_t>(k + 1) * Cfg<D>::HS;
   }
 };
 
-// Warp-uniform value (lane 0's): lets ptxas keep loop bounds and the layer's bank
-// offset in uniform registers, so weight pairs are LDCU.128 c[bank][UR + imm]
-// operands of FFMA2 even inside the node loops.
-__device__ __forceinline__ int uni(int v) { return __shfl_sync(0xffffffffu, v, 0); }
-
-// One message-passing layer for the CTA's subdomain.  WT >= 0: the layer's slot
-// offset in the constant bank as a compile-time constant (every weight pair is an
-// immediate-addressed LDCU.128 feeding FFMA2 — the fast path); WT < 0: runtime
-// offset w_rt (used only by the rare big-subdomain kernel).
-//
-// Node loops run a uniform trip count: each warp handles NPT consecutive SELL
-// slices (32 local nodes each) per iteration, node t of lane = n0 + 32 t + lane,
-// so one weight load feeds NPT nodes.  Slice widths (max degree in the slice)
-// bound the edge loop; padding records point at the dummy Q row k (all -1e30),
-// whose 2 relu term is exactly 0.  Lanes past k recompute node k-1 (phase A,
-// identical store) or write the dummy h row k (phase B): no divergent branches,
-// so the weight loads stay uniform.
-template <int D, int MODE, int WT, int NPT>
-__device__ __forceinline__ void gnn_layer(int w_rt, int k, int warp, float* gq, float* gh,
-                                          float* gc, const float2* __restrict__ xy,
-                                          const float2* __restrict__ edges,
-                                          const int* __restrict__ slice_off,
-                                          const uint16_t* __restrict__ deg, float alpha,
-                                          int* bad, int layer_no) {
-  using C = Cfg<D>;
-  const int W = WT >= 0 ? WT : w_rt;
-  constexpr int NP2 = C::NP2, NPH = C::NPH;
-  const int lane = threadIdx.x & 31, nthr = blockDim.x;
-  const int step = NPT * nthr;
-  NodeState<D, MODE> ns(k, gq, gh, gc);
-  // ---- phase A: destination projections Q_t = [h_t, x_t, y_t] . WQ ----
-  for (int n0 = 32 * NPT * warp; n0 < k; n0 += step) {
-    float hin[NPT][D + 2];
-    int nn[NPT];
-#pragma unroll
-    for (int t = 0; t < NPT; ++t) {
-      nn[t] = min(n0 + 32 * t + lane, k - 1);
-      load_hxy<D>(ns.h + nn[t] * C::HS, __ldg(xy + nn[t]), hin[t]);
-    }
-    float2 q[NPT][NP2];
-#pragma unroll
-    for (int t = 0; t < NPT; ++t)
-#pragma unroll
-      for (int j = 0; j < NP2; ++j) q[t][j] = make_float2(0.f, 0.f);
-    mv2n<NPT, D + 2, NP2, C::OFF_WQ, C::D2P>(W, hin, q);
-#pragma unroll
-    for (int t = 0; t < NPT; ++t) {
-      float qs[C::QS];
-#pragma unroll
-      for (int j = 0; j < C::QS; ++j) qs[j] = 0.f;
-#pragma unroll
-      for (int j = 0; j < NP2; ++j) {
-        qs[2 * j] = q[t][j].x;
-        qs[2 * j + 1] = q[t][j].y;
-      }
-      store_vec<C::QS>(ns.q + nn[t] * C::QS, qs);
-    }
-  }
+// one layer, all slices of the CTA's subdomain (warp w: slices w, w + nwarps, ...)
+template <int D, int W>
+__device__ __forceinline__ void cta_layer(const SmemState<D>& ns, int k, int warp,
+                                          const float2* xy, const float2* edges,
+                                          const int* slice_off, const uint16_t* deg,
+                                          float alpha, int* bad, int layer_no) {
+  const int step = blockDim.x;
+  for (int n0 = 32 * warp; n0 < k; n0 += step) slice_q<D, W>(n0, k, ns.h, ns.q, xy);
   __syncthreads();
-  // ---- phase B: edge aggregation + node update ----
   int first_bad = 0;
-  const float2 dummy = make_float2(0.f, __int_as_float(k));
-  for (int n0 = 32 * NPT * warp; n0 < k; n0 += step) {
-    int nn[NPT], width[NPT];
-    float2 p[NPT][NP2], s[NPT][NP2];
-    const float2* ep[NPT];
-    {
-      float hin[NPT][D + 2];
-#pragma unroll
-      for (int t = 0; t < NPT; ++t) {
-        nn[t] = min(n0 + 32 * t + lane, k - 1);
-        load_hxy<D>(ns.h + nn[t] * C::HS, __ldg(xy + nn[t]), hin[t]);
-#pragma unroll
-        for (int j = 0; j < NP2; ++j) {
-          p[t][j] = cpair(W + C::OFF_B1 + 2 * j);
-          s[t][j] = make_float2(0.f, 0.f);
-        }
-      }
-      mv2n<NPT, D + 2, NP2, C::OFF_WP, C::D2P>(W, hin, p);
-    }
-    int wmax = 0;
-#pragma unroll
-    for (int t = 0; t < NPT; ++t) {
-      const int q = (n0 >> 5) + t;
-      const bool live = n0 + 32 * t < k;  // warp-uniform
-      const int so = uni(slice_off[live ? q : 0]);
-      width[t] = live ? (uni(slice_off[q + 1]) - so) >> 5 : 0;
-      ep[t] = edges + so + lane;
-      wmax = max(wmax, width[t]);
-    }
-    float2 rec[NPT];
-#pragma unroll
-    for (int t = 0; t < NPT; ++t) rec[t] = width[t] > 0 ? __ldg(ep[t]) : dummy;
-    for (int e = 0; e < wmax; ++e) {
-      float2 cur[NPT];
-#pragma unroll
-      for (int t = 0; t < NPT; ++t) {
-        cur[t] = rec[t];
-        rec[t] = e + 1 < width[t] ? __ldg(ep[t] + 32 * (e + 1)) : dummy;
-      }
-#pragma unroll
-      for (int t = 0; t < NPT; ++t) {
-        float qt[C::QS];
-        load_vec<C::QS>(ns.q + __float_as_int(cur[t].y) * C::QS, qt);
-        const float2 len = bcast(cur[t].x);
-#pragma unroll
-        for (int j = 0; j < NP2; ++j) {
-          float2 x = fadd2(p[t][j], make_float2(qt[2 * j], qt[2 * j + 1]));
-          x = ffma2(len, cpair(W + C::OFF_WL + 2 * j), x);
-          s[t][j] = fadd2(s[t][j], relu2x(x));
-        }
-      }
-    }
-    // psi first layer with the messages' second layer folded in
-    float2 u[NPT][NPH];
-    float hc[NPT][D + 2];
-#pragma unroll
-    for (int t = 0; t < NPT; ++t) {
-#pragma unroll
-      for (int j = 0; j < NPH; ++j) u[t][j] = cpair(W + C::OFF_BP1 + 2 * j);
-      float hv[C::DH];
-      load_vec<C::DH>(ns.h + nn[t] * C::HS, hv);
-#pragma unroll
-      for (int i = 0; i < D; ++i) hc[t][i] = hv[i];
-      hc[t][D] = ns.c[nn[t]];
-      hc[t][D + 1] = static_cast<float>(deg[nn[t]]);
-    }
-    mv2n<NPT, D + 2, NPH, C::OFF_WU, C::DP>(W, hc, u);
-    {
-      float sv[NPT][2 * D];
-#pragma unroll
-      for (int t = 0; t < NPT; ++t)
-#pragma unroll
-        for (int j = 0; j < NP2; ++j) {
-          sv[t][2 * j] = s[t][j].x;
-          sv[t][2 * j + 1] = s[t][j].y;
-        }
-      // second, independent accumulator chain for the message part (ILP)
-      float2 u2[NPT][NPH];
-#pragma unroll
-      for (int t = 0; t < NPT; ++t)
-#pragma unroll
-        for (int j = 0; j < NPH; ++j) u2[t][j] = make_float2(0.f, 0.f);
-      mv2n<NPT, 2 * D, NPH, C::OFF_WU + (D + 2) * C::DP, C::DP>(W, sv, u2);
-#pragma unroll
-      for (int t = 0; t < NPT; ++t)
-#pragma unroll
-        for (int j = 0; j < NPH; ++j) u[t][j] = fadd2(u[t][j], u2[t][j]);
-    }
-    float uv[NPT][D];
-    float2 o[NPT][NPH];
-#pragma unroll
-    for (int t = 0; t < NPT; ++t)
-#pragma unroll
-      for (int j = 0; j < NPH; ++j) {
-        const float2 r2 = relu2x(u[t][j]);
-        if (2 * j < D) uv[t][2 * j] = r2.x;
-        if (2 * j + 1 < D) uv[t][2 * j + 1] = r2.y;
-        o[t][j] = cpair(W + C::OFF_BP2 + 2 * j);
-      }
-    mv2n<NPT, D, NPH, C::OFF_WP2, C::DP>(W, uv, o);
-    const float2 al = bcast(alpha);
-#pragma unroll
-    for (int t = 0; t < NPT; ++t) {
-      const int n = n0 + 32 * t + lane;
-      float hn[C::DH];
-      float2 fin = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int j = 0; j < NPH; ++j) {
-        float2 hp = make_float2(hc[t][2 * j], 2 * j + 1 < D ? hc[t][2 * j + 1] : 0.f);
-        hp = ffma2(al, o[t][j], hp);
-        fin = ffma2(hp, make_float2(0.f, 0.f), fin);  // NaN iff some h is non-finite (dss.py:324)
-        hn[2 * j] = hp.x;
-        hn[2 * j + 1] = (2 * j + 1 < D) ? hp.y : 0.f;
-      }
-      if ((fin.x != 0.f || fin.y != 0.f) && first_bad == 0 && n < k) first_bad = layer_no;
-      // every thread of the warp has read its nodes' h above (same iteration), so the
-      // in-place update cannot race; lanes past k write the dummy row k
-      store_vec<C::DH>(ns.h + min(n, k) * C::HS, hn);
-    }
+  for (int n0 = 32 * warp; n0 < k; n0 += step) {
+    const int so = uni(slice_off[n0 >> 5]);
+    const int width = (uni(slice_off[(n0 >> 5) + 1]) - so) >> 5;
+    float hn[Cfg<D>::DH];
+    const bool b = slice_u<D, W>(n0, k, ns.h, ns.q, ns.c, xy, edges, so, width, deg, alpha, hn);
+    if (b && first_bad == 0) first_bad = layer_no;
   }
   if (first_bad != 0 && *bad == 0) *bad = first_bad;
   __syncthreads();
@@ -356,136 +316,117 @@ struct GnnShared {
   double scale;
 };
 
-template <int D, int MODE, bool SLOTS, int NPT>
-__device__ __forceinline__ void gnn_body(const GnnArgs& a, GnnShared& sh, int sub, int pos0,
-                                         int k) {
-  using C = Cfg<D>;
-  constexpr bool SV = MODE == 0;  // node state fully in shared memory
+// Restriction of r to subdomain `sub` (hybrid.py:103-108) and its coarse RHS row
+// (R0 r)_i, by the whole CTA: writes scale/r0r, c (fp32 r_i / s_i) into c_out and
+// zeroes h rows 0..k-1.  Returns s_i (uniform).
+template <int D>
+__device__ __forceinline__ double restrict_sub(const GnnArgs& a, GnnShared& sh, int sub,
+                                               int pos0, int k, double* scratch, float* c_out,
+                                               float* h) {
   const int tid = threadIdx.x, nthr = blockDim.x;
-  // global Q scratch keeps one extra (dummy) row per subdomain
-  float* gq = MODE == 2 ? a.qbuf + static_cast<size_t>(pos0 + sub) * C::QS : nullptr;
-  float* gh = MODE >= 1 ? a.hbuf + static_cast<size_t>(pos0 + sub) * C::HS : nullptr;
-  float* gc = MODE >= 1 ? a.cbuf + pos0 : nullptr;
-  NodeState<D, MODE> ns(k, gq, gh, gc);
-  double (&red)[2][kGnnThreads / 32] = sh.red;
-  int& sh_bad = sh.bad;
-  double& sh_scale = sh.scale;
-  if (tid == 0) sh_bad = 0;
+  double ss = 0.0, rr0 = 0.0;
+  for (int n = tid; n < k; n += nthr) {
+    const int g = a.idx[pos0 + n];
+    const double v = a.r[g];
+    ss = fma(v, v, ss);
+    rr0 = fma(a.pou[g], v, rr0);
+    scratch[n] = v;
+  }
+  ss = warp_sum(ss);
+  rr0 = warp_sum(rr0);
+  if ((tid & 31) == 0) {
+    sh.red[0][tid >> 5] = ss;
+    sh.red[1][tid >> 5] = rr0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double t0 = 0.0, t1 = 0.0;
+    for (int w = 0; w < (nthr >> 5); ++w) {
+      t0 += sh.red[0][w];
+      t1 += sh.red[1][w];
+    }
+    const double sc = sqrt(t0);
+    sh.scale = sc;
+    a.scale[sub] = sc;
+    a.r0r[sub] = t1;
+  }
+  __syncthreads();
+  const double s = __shfl_sync(0xffffffffu, sh.scale, 0);
+  if (s == 0.0) return s;  // zero local residual: the subdomain contributes nothing
+  for (int n = tid; n < k; n += nthr) c_out[n] = static_cast<float>(scratch[n] / s);
+  __syncthreads();  // scratch may alias Q
+  for (int n = tid; n < k; n += nthr) {
+    float z[Cfg<D>::DH];
+#pragma unroll
+    for (int i = 0; i < Cfg<D>::DH; ++i) z[i] = 0.f;
+    store_vec<Cfg<D>::DH>(h + n * Cfg<D>::HS, z);
+  }
+  return s;
+}
 
+// Subdomains whose node state fits the launch's shared memory (k <= a.cap0): one
+// CTA per subdomain (LPT order), the whole chunk of layers on chip.
+template <int D>
+__global__ void __launch_bounds__(kGnnThreads, 1) gnn_kernel(GnnArgs a) {
+  using C = Cfg<D>;
+  if (a.skip != nullptr && uni(*a.skip) != 0) return;
+  __shared__ GnnShared sh;
+  const int sub = uni(a.order[a.order_begin + blockIdx.x]);
+  const int pos0 = uni(a.sub_ptr[sub]);
+  const int k = uni(a.sub_ptr[sub + 1] - pos0);
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  SmemState<D> ns(k);
+  if (tid == 0) sh.bad = 0;
   double s;
   if (a.first) {
-    // ---- restriction (hybrid.py:103-108) and coarse RHS row (R0 r)_i ----
-    double* scratch = reinterpret_cast<double*>(ns.q);  // k doubles fit in k*QS floats
-    double ss = 0.0, rr0 = 0.0;
-    for (int n = tid; n < k; n += nthr) {
-      const int g = a.idx[pos0 + n];
-      const double v = a.r[g];
-      ss = fma(v, v, ss);
-      rr0 = fma(a.pou[g], v, rr0);
-      scratch[n] = v;
-    }
-    ss = warp_sum(ss);
-    rr0 = warp_sum(rr0);
-    if ((tid & 31) == 0) {
-      red[0][tid >> 5] = ss;
-      red[1][tid >> 5] = rr0;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      double t0 = 0.0, t1 = 0.0;
-      for (int w = 0; w < (nthr >> 5); ++w) {
-        t0 += red[0][w];
-        t1 += red[1][w];
-      }
-      const double sc = sqrt(t0);
-      sh_scale = sc;
-      a.scale[sub] = sc;
-      a.r0r[sub] = t1;
-    }
-    __syncthreads();
-    s = __shfl_sync(0xffffffffu, sh_scale, 0);
-    if (s == 0.0) {  // zero local residual: the subdomain contributes nothing
+    s = restrict_sub<D>(a, sh, sub, pos0, k, reinterpret_cast<double*>(ns.q), ns.c, ns.h);
+    if (s == 0.0) {
       if (tid == 0) {
         a.bad_layer[sub] = 0;
         a.out_bad[sub] = 0;
       }
       return;
     }
-    for (int n = tid; n < k; n += nthr) {
-      const float c = static_cast<float>(scratch[n] / s);
-      ns.c[n] = c;
-      if (SV && !a.last) a.cbuf[pos0 + n] = c;
-    }
-    __syncthreads();  // scratch (aliasing Q) fully consumed
-    for (int n = tid; n < k; n += nthr) {
-      float z[C::DH];
-#pragma unroll
-      for (int i = 0; i < C::DH; ++i) z[i] = 0.f;
-      store_vec<C::DH>(ns.h + n * C::HS, z);
-    }
-  } else {
+    if (!a.last)
+      for (int n = tid; n < k; n += nthr) a.cbuf[pos0 + n] = ns.c[n];
+  } else {  // later chunk of a deep model: reload the node state
     s = __shfl_sync(0xffffffffu, a.scale[sub], 0);
     if (s == 0.0) return;
-    if constexpr (SV) {
-      for (int n = tid; n < k; n += nthr) {
-        ns.c[n] = a.cbuf[pos0 + n];
-        float hv[C::DH];
-        load_vec<C::DH>(a.hbuf + static_cast<size_t>(pos0 + sub + n) * C::HS, hv);
-        store_vec<C::DH>(ns.h + n * C::HS, hv);
-      }
+    for (int n = tid; n < k; n += nthr) {
+      ns.c[n] = a.cbuf[pos0 + n];
+      float hv[C::DH];
+      load_vec<C::DH>(a.hbuf + static_cast<size_t>(pos0 + sub + n) * C::HS, hv);
+      store_vec<C::DH>(ns.h + n * C::HS, hv);
     }
   }
-  // dummy Q row k: target of the SELL padding records (2 relu(P - 1e30) == 0)
   for (int j = tid; j < C::QS; j += nthr) ns.q[static_cast<size_t>(k) * C::QS + j] = -1e30f;
   __syncthreads();
-
   {
     const int warp = uni(tid >> 5);
     const float2* xy = a.xy + pos0;
     const int* so = a.slice_off + a.slice_base[sub];
     const uint16_t* dg = a.deg + pos0;
-    if constexpr (SLOTS) {
-      // compile-time bank slots (LMAX <= 10)
 #define DDM_LAYER(LL)                                                                        \
   if constexpr (LL < C::LMAX) {                                                              \
     if (LL < a.nl)                                                                           \
-      gnn_layer<D, MODE, LL * C::STRIDE, NPT>(0, k, warp, gq, gh, gc, xy, a.edges, so, dg, a.alpha, \
-                                         &sh_bad, a.layer0 + LL);                            \
+      cta_layer<D, LL * C::STRIDE>(ns, k, warp, xy, a.edges, so, dg, a.alpha, &sh.bad,       \
+                                   a.layer0 + LL);                                           \
   }
-      DDM_LAYER(0) DDM_LAYER(1) DDM_LAYER(2) DDM_LAYER(3) DDM_LAYER(4)
-      DDM_LAYER(5) DDM_LAYER(6) DDM_LAYER(7) DDM_LAYER(8) DDM_LAYER(9)
+    DDM_LAYER(0) DDM_LAYER(1) DDM_LAYER(2) DDM_LAYER(3) DDM_LAYER(4)
+    DDM_LAYER(5) DDM_LAYER(6) DDM_LAYER(7) DDM_LAYER(8) DDM_LAYER(9)
 #undef DDM_LAYER
-    } else {
-#pragma unroll 1
-      for (int l = 0; l < a.nl; ++l)
-        gnn_layer<D, MODE, -1, NPT>(l * C::STRIDE, k, warp, gq, gh, gc, xy, a.edges, so, dg, a.alpha,
-                               &sh_bad, a.layer0 + l);
-    }
   }
-
   int outbad = 0;
   if (a.last) {
-    // ---- decoder of the final layer (dss.py:327) and rescaling (hybrid.py:135) ----
+    // decoder of the final layer (dss.py:327) and rescaling (hybrid.py:135)
     for (int n = tid; n < k; n += nthr) {
       float hv[C::DH];
       load_vec<C::DH>(ns.h + n * C::HS, hv);
-      float h[D];
-#pragma unroll
-      for (int i = 0; i < D; ++i) h[i] = hv[i];
-      float2 u[C::NPH];
-#pragma unroll
-      for (int j = 0; j < C::NPH; ++j) u[j] = cpair(C::DEC_B1 + 2 * j);
-      mv2<D, C::NPH, C::DEC_W1, C::DP>(0, h, u);
-      float o = c_w[C::DEC_B2];
-#pragma unroll
-      for (int i = 0; i < D; ++i) {
-        const float ui = (i & 1) ? u[i >> 1].y : u[i >> 1].x;
-        o = fmaf(relu_nan(ui), c_w[C::DEC_W2 + i], o);
-      }
+      const float o = decode<D>(hv);
       if (!isfinite(o)) outbad = 1;
       a.zloc[pos0 + n] = s * static_cast<double>(o);
     }
-  } else if constexpr (SV) {
+  } else {
     for (int n = tid; n < k; n += nthr) {
       float hv[C::DH];
       load_vec<C::DH>(ns.h + n * C::HS, hv);
@@ -494,7 +435,7 @@ __device__ __forceinline__ void gnn_body(const GnnArgs& a, GnnShared& sh, int su
   }
   outbad = __syncthreads_or(outbad);
   if (tid == 0) {
-    const int b = sh_bad;
+    const int b = sh.bad;
     if (a.first) {
       a.bad_layer[sub] = b;
       a.out_bad[sub] = outbad;
@@ -506,32 +447,88 @@ __device__ __forceinline__ void gnn_body(const GnnArgs& a, GnnShared& sh, int su
   }
 }
 
-// Subdomains whose node state (h, Q, c) fits the launch's shared memory (k <=
-// a.cap0): one CTA per subdomain in LPT order, compile-time bank slots.
+// ---------------------------------------------------------------------------- flat path
+// Subdomains too large for one CTA's shared memory (k > a.cap0): node-parallel,
+// one launch per phase per layer over all their slices (warp = slice, listed in
+// a.bslices as (subdomain, slice)), node state in global scratch (L2-resident):
+// h rows at hbuf[(pos0 + sub) ...], Q rows at qbuf[(pos0 + sub) ...] (each with a
+// dummy row k), c at cbuf[pos0 ...].  Same per-node arithmetic as the CTA path.
+
+// restriction of every big subdomain (CTA per subdomain, order[order_begin ...])
 template <int D>
-__global__ void __launch_bounds__(kGnnThreads / kGnnNpt, 1) gnn_kernel(GnnArgs a) {
+__global__ void __launch_bounds__(kGnnThreads, 1) gnn_flat_prologue(GnnArgs a) {
+  using C = Cfg<D>;
   if (a.skip != nullptr && uni(*a.skip) != 0) return;
   __shared__ GnnShared sh;
   const int sub = uni(a.order[a.order_begin + blockIdx.x]);
   const int pos0 = uni(a.sub_ptr[sub]);
   const int k = uni(a.sub_ptr[sub + 1] - pos0);
-  gnn_body<D, 0, true, kGnnNpt>(a, sh, sub, pos0, k);
+  float* h = a.hbuf + static_cast<size_t>(pos0 + sub) * C::HS;
+  float* q = a.qbuf + static_cast<size_t>(pos0 + sub) * C::QS;
+  // restriction scratch: k doubles in the subdomain's Q rows (k*QS floats >= 2k)
+  const double s = restrict_sub<D>(a, sh, sub, pos0, k, reinterpret_cast<double*>(q),
+                                   a.cbuf + pos0, h);
+  if (threadIdx.x == 0) {
+    a.bad_layer[sub] = 0;
+    a.out_bad[sub] = 0;
+  }
+  if (s == 0.0) return;
+  for (int j = threadIdx.x; j < C::QS; j += blockDim.x) q[static_cast<size_t>(k) * C::QS + j] = -1e30f;
 }
 
-// The few oversized subdomains (k > a.cap0): Q alone in shared memory (k <= a.cap1,
-// compile-time bank slots) or everything in global scratch (runtime bank slots).  Launched concurrently with
-// gnn_kernel on a side stream (gnn.cu).
 template <int D>
-__global__ void __launch_bounds__(kGnnThreads, 1) gnn_big_kernel(GnnArgs a) {
+struct FlatSlice {
+  int sub, pos0, k, n0;
+  double s;
+  __device__ __forceinline__ explicit FlatSlice(const GnnArgs& a) {
+    const int2 bs = a.bslices[blockIdx.x];
+    sub = uni(bs.x);
+    n0 = uni(bs.y) * 32;
+    pos0 = uni(a.sub_ptr[sub]);
+    k = uni(a.sub_ptr[sub + 1] - pos0);
+    s = __shfl_sync(0xffffffffu, a.scale[sub], 0);
+  }
+};
+
+template <int D, int W>
+__global__ void __launch_bounds__(32) gnn_flat_q(GnnArgs a) {
+  using C = Cfg<D>;
   if (a.skip != nullptr && uni(*a.skip) != 0) return;
-  __shared__ GnnShared sh;
-  const int sub = uni(a.order[a.order_begin + blockIdx.x]);
-  const int pos0 = uni(a.sub_ptr[sub]);
-  const int k = uni(a.sub_ptr[sub + 1] - pos0);
-  if (k <= a.cap1) {
-    gnn_body<D, 1, true, 1>(a, sh, sub, pos0, k);
-  } else {
-    gnn_body<D, 2, false, 1>(a, sh, sub, pos0, k);
+  const FlatSlice<D> f(a);
+  if (f.s == 0.0) return;
+  slice_q<D, W>(f.n0, f.k, a.hbuf + static_cast<size_t>(f.pos0 + f.sub) * C::HS,
+                a.qbuf + static_cast<size_t>(f.pos0 + f.sub) * C::QS, a.xy + f.pos0);
+}
+
+template <int D, int W>
+__global__ void __launch_bounds__(32) gnn_flat_u(GnnArgs a, int layer_no, int decode_last) {
+  using C = Cfg<D>;
+  if (a.skip != nullptr && uni(*a.skip) != 0) return;
+  const FlatSlice<D> f(a);
+  if (f.s == 0.0) return;
+  const int* so_p = a.slice_off + a.slice_base[f.sub] + (f.n0 >> 5);
+  const int so = uni(so_p[0]);
+  const int width = (uni(so_p[1]) - so) >> 5;
+  float hn[C::DH];
+  const bool bad = slice_u<D, W>(f.n0, f.k, a.hbuf + static_cast<size_t>(f.pos0 + f.sub) * C::HS,
+                                 a.qbuf + static_cast<size_t>(f.pos0 + f.sub) * C::QS,
+                                 a.cbuf + f.pos0, a.xy + f.pos0, a.edges, so, width,
+                                 a.deg + f.pos0, a.alpha, hn);
+  // layers run in order (one launch each), so the first non-zero wins
+  if (bad) {
+    atomicCAS(&a.bad_layer[f.sub], 0, layer_no);
+    atomicMax(a.status, static_cast<int>(kPrecondError));
+  }
+  if (decode_last) {
+    const int n = f.n0 + static_cast<int>(threadIdx.x & 31);
+    const float o = decode<D>(hn);
+    if (n < f.k) {
+      if (!isfinite(o)) {
+        a.out_bad[f.sub] = 1;
+        atomicMax(a.status, static_cast<int>(kPrecondError));
+      }
+      a.zloc[f.pos0 + n] = f.s * static_cast<double>(o);
+    }
   }
 }
 
