@@ -149,6 +149,46 @@ def test_large_subdomains_use_global_variant(ddm):
     assert rel_l2(p(g["r"]), ref(g["r"])) < TOL
 
 
+def _merged_config_a(ddm):
+    g = load_golden("A.npz")
+    a, _b, coords, dec = _dec(ddm, g)
+    merged = [np.union1d(np.union1d(dec.subdomains[0], dec.subdomains[1]), dec.subdomains[2]),
+              np.union1d(dec.subdomains[3], dec.subdomains[4])]
+    return g, a, coords, ddm.finish_decomposition(merged, dec.base_owner, dec.overlap), merged
+
+
+@pytest.mark.parametrize("k_bar", [10, 30])
+def test_flat_path_two_level_deep_model(ddm, k_bar):
+    """Oversized subdomains (flat node-parallel path), two-level, and a model deep
+    enough for several constant-bank chunks, against the oracle."""
+    from oracle import ddm_oracle as orc
+
+    g, a, coords, dec2, merged = _merged_config_a(ddm)
+    model = ddm.init_model(k_bar, 10, seed=2)
+    p = ddm.build_ddm_gnn(a, coords, dec2, model, level="two")
+    info = p.info()
+    assert info["n_big"] >= 1 and (k_bar < 11 or info["n_chunks"] > 1)
+    om = orc.model_from_flat(k_bar, 10, model.alpha, 2, ddm.flat_params(model))
+    ref = orc.OraclePreconditioner(a, coords, merged, om, "two")
+    assert rel_l2(p(g["r"]), ref(g["r"])) < TOL
+    assert np.array_equal(p(g["r"]), p(g["r"]))
+
+
+def test_flat_path_reports_non_finite_states(ddm):
+    g, a, coords, dec2, _merged = _merged_config_a(ddm)
+    model = ddm.init_model(3, 10, seed=1)
+    model.layers[1].psi.b2[...] = np.inf
+    p = ddm.build_ddm_gnn(a, coords, dec2, model)
+    assert p.info()["n_big"] >= 1
+    with pytest.raises(RuntimeError, match="non-finite latent state at message-passing iteration 2"):
+        p(g["r"])
+    model = ddm.init_model(2, 10, seed=4)
+    model.layers[-1].dec.w2[...] = np.nan
+    p = ddm.build_ddm_gnn(a, coords, dec2, model)
+    with pytest.raises(RuntimeError, match="non-finite model output in subdomain 0"):
+        p(g["r"])
+
+
 # ---------------------------------------------------------------- invariants
 
 
