@@ -54,6 +54,12 @@ enum DevStatus : int {
 #endif
 constexpr int kGnnThreads = GNN_THREADS;  // GNN CTA size (28 warps/SM; measured best of 640-1024)
 constexpr int kConstFloats = 16384;  // 64 KB constant bank
+#ifndef GNN_TC_Q
+#define GNN_TC_Q 0  // phase-A projection on tcgen05 (3xTF32) instead of FFMA2
+#endif
+// shared memory reserved at the start of the CTA path's dynamic smem for the
+// tensor-core B operand (WQ^T hi/lo, 2 x 32 x 16 fp32)
+constexpr int kTcSmemBytes = GNN_TC_Q ? 4096 : 0;
 constexpr int kGnnSmemMax = 227 * 1024 - 1024;  // dynamic smem cap (static smem < 1 KB)
 
 struct DeviceLayout {

@@ -105,14 +105,13 @@ size_t gnn_plan_smem(int d, int k_max, int* cap0, int* cap1) {
   }
   const int node1 = 4 * qs;                            // Q only
   // +1 node: the dummy Q row addressed by SELL padding records
-  const size_t m0 = static_cast<size_t>(k_max + 1) * node0;
+  const size_t m0 = static_cast<size_t>(k_max + 1) * node0 + kTcSmemBytes;
   const size_t m1 = static_cast<size_t>(k_max + 1) * node1;
   size_t smem;
   if (m0 <= static_cast<size_t>(kGnnSmemMax)) smem = m0;
-  else if (m1 <= static_cast<size_t>(kGnnSmemMax)) smem = kGnnSmemMax;  // mixed modes 0/1
   else smem = kGnnSmemMax;
-  *cap0 = node0 ? static_cast<int>(smem / node0) - 1 : 0;
-  *cap1 = node1 ? static_cast<int>(smem / node1) - 1 : 0;
+  *cap0 = node0 ? static_cast<int>((smem - kTcSmemBytes) / node0) - 1 : 0;
+  *cap1 = node1 ? static_cast<int>(m1 / node1) - 1 : 0;
   // restriction scratch (k doubles) aliases Q: guaranteed since QS >= 2
   return smem;
 }

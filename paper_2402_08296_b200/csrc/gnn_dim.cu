@@ -39,9 +39,11 @@ cudaError_t DDM_NAME(gnn_configure)() {
 // largest subdomain of the launch, smem = dynamic shared memory chosen by the host.
 cudaError_t DDM_NAME(gnn_launch)(int n_ctas, int k_max, size_t smem, const GnnArgs& a,
                                  cudaStream_t s) {
-  int threads = ((k_max + 31) / 32) * 32;
-  if (threads > kGnnThreads) threads = kGnnThreads;
-  if (threads < 64) threads = 64;
+  // tensor-core groups are 4 warps (one per TMEM lane quarter): multiples of 128
+  constexpr int gran = GNN_TC_Q ? 128 : 32;
+  int threads = ((k_max + gran - 1) / gran) * gran;
+  if (threads > kGnnThreads) threads = kGnnThreads / gran * gran;
+  if (threads < 128) threads = 128;
   gnn_kernel<GNN_D><<<n_ctas, threads, smem, s>>>(a);
   return cudaGetLastError();
 }

@@ -275,22 +275,176 @@ __device__ __forceinline__ float decode(const float (&hv)[Cfg<D>::DH]) {
 template <int D>
 struct SmemState {
   float *q, *h, *c;
+  unsigned char* tc;  // tensor-core staging (kTcSmemBytes) when GNN_TC_Q
   __device__ __forceinline__ explicit SmemState(int k) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    q = reinterpret_cast<float*>(smem_raw);
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    tc = smem_raw;
+    q = reinterpret_cast<float*>(smem_raw + kTcSmemBytes);
     h = q + static_cast<size_t>(k + 1) * Cfg<D>::QS;
     c = h + static_cast<size_t>(k + 1) * Cfg<D>::HS;
   }
 };
+
+// ---------------------------------------------------------------------------- tcgen05
+// Phase A on the 5th-generation tensor cores (GNN_TC_Q): Q = [h, x, y] . WQ for a
+// 128-node tile as one tcgen05.mma kind::tf32 GEMM (M=128, N=32 >= 2d, K=16 >=
+// d+2), in 3xTF32 (a_hi b_hi + a_hi b_lo + a_lo b_hi: fp32-level accuracy,
+// tools/ubench/tc_tf32_test.cu).  A (the tile's [h,x,y] split into tf32 hi/lo)
+// is written to TMEM by the four warps that own the tile's 32-row lane quarters
+// (tcgen05.st), B (WQ^T hi/lo, K-major, SWIZZLE_NONE) sits in shared memory, the
+// fp32 accumulator in TMEM is read back with tcgen05.ld and stored as Q rows.
+// Groups of four warps (7 at 28 warps) work on their tiles independently
+// (named barrier + one mbarrier per group).
+#if GNN_TC_Q
+constexpr int kTcK = 16, kTcN = 32;
+constexpr int kTcGroupCols = 64;  // per group: A_hi 16 | A_lo 16 | D 32 TMEM columns
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// K-major SWIZZLE_NONE canonical layout: core matrix = 8 rows x 16 B
+__device__ __forceinline__ int tc_kmaj(int r, int k) {
+  return (r >> 3) * ((kTcK / 4) * 128) + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4;
+}
+__device__ __forceinline__ uint64_t tc_sdesc(uint32_t addr) {
+  return static_cast<uint64_t>((addr >> 4) & 0x3FFF) |
+         (static_cast<uint64_t>(128 >> 4) << 16) |                     // LBO: next K core
+         (static_cast<uint64_t>(((kTcK / 4) * 128) >> 4) << 32) |      // SBO: next 8 rows
+         (static_cast<uint64_t>(1) << 46);                             // sm_100 version
+}
+constexpr uint32_t kTcIdesc = (1u << 4) | (2u << 7) | (2u << 10) |
+                              (static_cast<uint32_t>(kTcN >> 3) << 17) | (8u << 24);
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+__device__ __forceinline__ void tc_st16(uint32_t taddr, const float (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+      "%13,%14,%15,%16};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]),
+      "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]),
+      "f"(v[15]));
+}
+__device__ __forceinline__ void tc_ld16(uint32_t taddr, float (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
+        "=f"(v[7]), "=f"(v[8]), "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]),
+        "=f"(v[14]), "=f"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tc_ld4(uint32_t taddr, float (&v)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tc_mma(uint32_t d, uint32_t a, uint64_t b, int acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %4, p;\n\t}\n"
+      ::"r"(d), "r"(a), "l"(b), "r"(acc), "r"(kTcIdesc));
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tTC_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra TC_DONE;\n\tbra TC_WAIT;\n\tTC_DONE:\n\t}" ::"r"(mbar), "r"(parity));
+}
+
+// B operand of layer slot W: WQ^T split into tf32 hi/lo, K-major, into tc (whole CTA)
+template <int D, int W>
+__device__ __forceinline__ void tc_stage_wq(unsigned char* tc) {
+  using C = Cfg<D>;
+  float* bh = reinterpret_cast<float*>(tc);
+  float* bl = bh + kTcN * kTcK;
+  for (int i = threadIdx.x; i < kTcN * kTcK; i += blockDim.x) {
+    const int n = i / kTcK, k = i % kTcK;
+    const float w = (n < 2 * D && k < D + 2) ? c_w[W + C::OFF_WQ + k * C::D2P + n] : 0.f;
+    const float hi = tf32_rna(w);
+    bh[tc_kmaj(n, k) >> 2] = hi;
+    bl[tc_kmaj(n, k) >> 2] = tf32_rna(w - hi);
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+}
+
+// phase A of one layer on the tensor cores, all tiles of the subdomain
+template <int D>
+__device__ __forceinline__ void tc_phase_q(int k, int warp, uint32_t tmem, unsigned char* tc,
+                                           uint64_t* mbar, uint32_t& uses, const float* h,
+                                           float* q, const float2* __restrict__ xy) {
+  using C = Cfg<D>;
+  static_assert(2 * D <= kTcN && D + 2 <= kTcK, "tile shape");
+  const int lane = threadIdx.x & 31, quarter = warp & 3, group = warp >> 2;
+  const int ngroups = blockDim.x >> 7;
+  const uint32_t cols = tmem + group * kTcGroupCols;
+  const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
+  const uint32_t b_hi = smem_u32(tc), b_lo = b_hi + kTcN * kTcK * 4;
+  const uint32_t mb = smem_u32(&mbar[group]);
+  const int ntiles = (k + 127) >> 7;
+  for (int t = group; t < ntiles; t += ngroups) {
+    const int nn = min(t * 128 + quarter * 32 + lane, k - 1);
+    float hin[D + 2];
+    load_hxy<D>(h + nn * C::HS, __ldg(xy + nn), hin);
+    float ahi[16], alo[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float x = i < D + 2 ? hin[i] : 0.f;
+      ahi[i] = tf32_rna(x);
+      alo[i] = tf32_rna(x - ahi[i]);
+    }
+    tc_st16(cols + lane_base, ahi);
+    tc_st16(cols + lane_base + 16, alo);
+    asm volatile("tcgen05.wait::st.sync.aligned;");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    asm volatile("bar.sync %0, 128;" ::"r"(1 + group));
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (quarter == 0 && lane == 0) {
+      const uint32_t d = cols + 32;
+#pragma unroll
+      for (int ks = 0; ks < kTcK / 8; ++ks) {
+        tc_mma(d, cols + 8 * ks, tc_sdesc(b_hi + ks * 256), ks > 0);      // a_hi b_hi
+        tc_mma(d, cols + 8 * ks, tc_sdesc(b_lo + ks * 256), 1);           // a_hi b_lo
+        tc_mma(d, cols + 16 + 8 * ks, tc_sdesc(b_hi + ks * 256), 1);      // a_lo b_hi
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                   ::"r"(mb));
+    }
+    mbar_wait(mb, uses & 1);
+    ++uses;
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    float v0[16], v1[4];
+    tc_ld16(cols + lane_base + 32, v0);
+    tc_ld4(cols + lane_base + 48, v1);
+    asm volatile("tcgen05.wait::ld.sync.aligned;");
+    float qs[C::QS];
+#pragma unroll
+    for (int j = 0; j < C::QS; ++j) qs[j] = j < 16 ? v0[j] : (j < 20 ? v1[j - 16] : 0.f);
+#pragma unroll
+    for (int j = 2 * D; j < C::QS; ++j) qs[j] = 0.f;
+    store_vec<C::QS>(q + nn * C::QS, qs);
+    asm volatile("tcgen05.fence::before_thread_sync;");
+  }
+}
+#endif
 
 // one layer, all slices of the CTA's subdomain (warp w: slices w, w + nwarps, ...)
 template <int D, int W>
 __device__ __forceinline__ void cta_layer(const SmemState<D>& ns, int k, int warp,
                                           const float2* xy, const float2* edges,
                                           const int* slice_off, const uint16_t* deg,
-                                          float alpha, int* bad, int layer_no) {
+                                          float alpha, int* bad, int layer_no,
+                                          uint32_t tmem, uint64_t* mbar, uint32_t& uses) {
   const int step = blockDim.x;
+#if GNN_TC_Q
+  tc_stage_wq<D, W>(ns.tc);
+  __syncthreads();
+  tc_phase_q<D>(k, warp, tmem, ns.tc, mbar, uses, ns.h, ns.q, xy);
+#else
   for (int n0 = 32 * warp; n0 < k; n0 += step) slice_q<D, W>(n0, k, ns.h, ns.q, xy);
+#endif
   __syncthreads();
   int first_bad = 0;
   for (int n0 = 32 * warp; n0 < k; n0 += step) {
@@ -314,6 +468,8 @@ struct GnnShared {
   double red[2][kGnnThreads / 32];
   int bad;
   double scale;
+  uint64_t mbar[kGnnThreads / 128];  // tensor-core groups (GNN_TC_Q)
+  uint32_t tmem;
 };
 
 // Restriction of r to subdomain `sub` (hybrid.py:103-108) and its coarse RHS row
@@ -401,6 +557,21 @@ __global__ void __launch_bounds__(kGnnThreads, 1) gnn_kernel(GnnArgs a) {
   }
   for (int j = tid; j < C::QS; j += nthr) ns.q[static_cast<size_t>(k) * C::QS + j] = -1e30f;
   __syncthreads();
+  uint32_t tmem = 0, uses = 0;
+#if GNN_TC_Q
+  if (tid < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;"
+                 ::"r"(smem_u32(&sh.tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid < (nthr >> 7))
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sh.mbar[tid])));
+  asm volatile("fence.mbarrier_init.release.cluster;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  tmem = sh.tmem;
+#endif
   {
     const int warp = uni(tid >> 5);
     const float2* xy = a.xy + pos0;
@@ -410,12 +581,17 @@ __global__ void __launch_bounds__(kGnnThreads, 1) gnn_kernel(GnnArgs a) {
   if constexpr (LL < C::LMAX) {                                                              \
     if (LL < a.nl)                                                                           \
       cta_layer<D, LL * C::STRIDE>(ns, k, warp, xy, a.edges, so, dg, a.alpha, &sh.bad,       \
-                                   a.layer0 + LL);                                           \
+                                   a.layer0 + LL, tmem, sh.mbar, uses);                      \
   }
     DDM_LAYER(0) DDM_LAYER(1) DDM_LAYER(2) DDM_LAYER(3) DDM_LAYER(4)
     DDM_LAYER(5) DDM_LAYER(6) DDM_LAYER(7) DDM_LAYER(8) DDM_LAYER(9)
 #undef DDM_LAYER
   }
+#if GNN_TC_Q
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+#endif
   int outbad = 0;
   if (a.last) {
     // decoder of the final layer (dss.py:327) and rescaling (hybrid.py:135)
