@@ -374,6 +374,7 @@ static int refresh_classes(ddmgnn_ctx* c) {
   CUDA_TRY(dalloc(&c->d_qbuf, nb ? (V + c->K) * qs : 0));
   dfree(c->d_bslices);
   c->n_bslices = static_cast<int>(bsl.size());
+  while (bsl.size() % kFlatWarps) bsl.push_back(make_int2(-1, 0));  // padding slices
   if (!bsl.empty()) CUDA_TRY(upload(&c->d_bslices, bsl));
   return kOk;
 }

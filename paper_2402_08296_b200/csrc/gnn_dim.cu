@@ -79,8 +79,9 @@ cudaError_t DDM_NAME(gnn_launch)(int n_subs, int /*k_max*/, size_t /*smem*/, con
   if (n_subs <= 0 || a.n_bslices <= 0) return cudaSuccess;
   if (a.first) gnn_flat_prologue<GNN_D><<<n_subs, kGnnThreads, 0, s>>>(a);
   for (int l = 0; l < a.nl; ++l) {
-    qk[l]<<<a.n_bslices, 32, 0, s>>>(a);
-    uk[l]<<<a.n_bslices, 32, 0, s>>>(a, a.layer0 + l, a.last && l == a.nl - 1);
+    const int blocks = (a.n_bslices + kFlatWarps - 1) / kFlatWarps;  // table padded
+    qk[l]<<<blocks, 32 * kFlatWarps, 0, s>>>(a);
+    uk[l]<<<blocks, 32 * kFlatWarps, 0, s>>>(a, a.layer0 + l, a.last && l == a.nl - 1);
   }
   return cudaGetLastError();
 }

@@ -656,18 +656,23 @@ template <int D>
 struct FlatSlice {
   int sub, pos0, k, n0;
   double s;
+  // warp w of CTA b takes slice b * kFlatWarps + w: consecutive slices of one
+  // subdomain share a CTA (and its L1) since neighbours' Q rows are mostly within
+  // a few slices; padding entries (sub = -1) make s = 0 (the warp exits)
   __device__ __forceinline__ explicit FlatSlice(const GnnArgs& a) {
-    const int2 bs = a.bslices[blockIdx.x];
+    const int2 bs = a.bslices[blockIdx.x * kFlatWarps + uni(static_cast<int>(threadIdx.x) >> 5)];
     sub = uni(bs.x);
+    const bool pad = sub < 0;
+    if (pad) sub = 0;
     n0 = uni(bs.y) * 32;
     pos0 = uni(a.sub_ptr[sub]);
     k = uni(a.sub_ptr[sub + 1] - pos0);
-    s = __shfl_sync(0xffffffffu, a.scale[sub], 0);
+    s = pad ? 0.0 : __shfl_sync(0xffffffffu, a.scale[sub], 0);
   }
 };
 
 template <int D, int W>
-__global__ void __launch_bounds__(32) gnn_flat_q(GnnArgs a) {
+__global__ void __launch_bounds__(32 * kFlatWarps) gnn_flat_q(GnnArgs a) {
   using C = Cfg<D>;
   if (a.skip != nullptr && uni(*a.skip) != 0) return;
   const FlatSlice<D> f(a);
@@ -677,7 +682,7 @@ __global__ void __launch_bounds__(32) gnn_flat_q(GnnArgs a) {
 }
 
 template <int D, int W>
-__global__ void __launch_bounds__(32) gnn_flat_u(GnnArgs a, int layer_no, int decode_last) {
+__global__ void __launch_bounds__(32 * kFlatWarps) gnn_flat_u(GnnArgs a, int layer_no, int decode_last) {
   using C = Cfg<D>;
   if (a.skip != nullptr && uni(*a.skip) != 0) return;
   const FlatSlice<D> f(a);
