@@ -133,6 +133,16 @@ int ddmgnn_axpy2(int64_t n, double alpha, const double* p, const double* q, doub
                  double* work, double* rr_out, void* stream);
 /* p = z + beta p (sparse.py:126). */
 int ddmgnn_xpby(int64_t n, const double* z, double beta, double* p, void* stream);
+/* Device-side scalars of the distributed PCG: st = {rho, pq, alpha, rr, nb, tol, rz,
+ * beta, iter, status, max_iter} (fp64, device).  op 0: alpha = rho / pq (status 3 if
+ * pq <= 0, sparse.py:108-111); op 1: rel = sqrt(rr) / nb, hist[++iter] = rel, status
+ * 1 converged / 2 max_iter / 4 non-finite (sparse.py:114-121); op 2: beta = rz / rho,
+ * rho = rz (sparse.py:123-125).  No-ops once status != 0. */
+int ddmgnn_pcg_scalars(int op, double* st, double* hist, void* stream);
+/* ddmgnn_axpy2 / ddmgnn_xpby with alpha / beta read from st (no-ops once status != 0). */
+int ddmgnn_axpy2_dev(int64_t n, const double* st, const double* p, const double* q, double* u,
+                     double* r, double* work, double* rr_out, void* stream);
+int ddmgnn_xpby_dev(int64_t n, const double* z, const double* st, double* p, void* stream);
 /* y = A x, A dense row-major k x k (the coarse inverse, sparse.py:163 / hybrid.py:117). */
 int ddmgnn_dense_gemv(int64_t k, const double* a, const double* x, double* y, void* stream);
 /* Gluing over a transpose map (hybrid.py:117,133-135): for DOF j < n,

@@ -69,6 +69,9 @@ SIGNATURES = [
     ("ddmgnn_axpy2", _int, [_i64, _dbl, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     ("ddmgnn_xpby", _int, [_i64, _vp, _dbl, _vp, _vp]),
     ("ddmgnn_dense_gemv", _int, [_i64, _vp, _vp, _vp, _vp]),
+    ("ddmgnn_pcg_scalars", _int, [_int, _vp, _vp, _vp]),
+    ("ddmgnn_axpy2_dev", _int, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    ("ddmgnn_xpby_dev", _int, [_i64, _vp, _vp, _vp, _vp]),
     ("ddmgnn_prolong", _int, [_i64, _int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
 ]
 

@@ -169,3 +169,88 @@ extern "C" int ddmgnn_prolong(int64_t n, int two_level, const int32_t* tptr,
                                     nullptr, nullptr, nullptr, 0, nullptr,
                                     static_cast<cudaStream_t>(stream)));
 }
+
+// ---------------------------------------------------------------- device-side scalars
+// Distributed PCG with its scalars on the device (no host round trip per dot):
+// st[] = {rho, pq, alpha, rr, nb, tol, rz, beta, iter, status, max_iter}; the
+// all-reduces of pq, rr, rz operate on st[1], st[3], st[6] in place, and the
+// updates below become no-ops once status != 0 (converged / not SPD / non-finite),
+// so the host only polls the status every few iterations.
+namespace ddmgnn {
+namespace {
+enum { kRho, kPq, kAlpha, kRr, kNb, kTol, kRz, kBeta, kIter, kStatus, kMaxIter };
+
+__global__ void pcg_scalars_kernel(int op, double* st, double* hist) {
+  if (st[kStatus] != 0.0) return;
+  if (op == 0) {  // alpha = rho / <p, Ap> (sparse.py:108-111)
+    if (st[kPq] <= 0.0) st[kStatus] = 3.0;
+    else st[kAlpha] = st[kRho] / st[kPq];
+  } else if (op == 1) {  // relative residual, history, stopping test (sparse.py:114-121)
+    const double rel = sqrt(st[kRr]) / st[kNb];
+    const int it = static_cast<int>(st[kIter]) + 1;
+    st[kIter] = it;
+    if (!isfinite(rel)) {
+      st[kStatus] = 4.0;
+      return;
+    }
+    hist[it] = rel;
+    if (rel < st[kTol]) st[kStatus] = 1.0;
+    else if (it >= static_cast<int>(st[kMaxIter])) st[kStatus] = 2.0;
+  } else {  // beta = rho' / rho, rho = rho' (sparse.py:123-125)
+    st[kBeta] = st[kRz] / st[kRho];
+    st[kRho] = st[kRz];
+  }
+}
+
+__global__ void axpy2_dev_kernel(long long n, const double* __restrict__ st,
+                                 const double* __restrict__ p, const double* __restrict__ q,
+                                 double* __restrict__ u, double* __restrict__ r,
+                                 double* __restrict__ part) {
+  double acc = 0.0;
+  if (st[kStatus] == 0.0) {
+    const double alpha = st[kAlpha];
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+      u[i] = __dadd_rn(u[i], __dmul_rn(alpha, p[i]));
+      const double ri = __dsub_rn(r[i], __dmul_rn(alpha, q[i]));
+      r[i] = ri;
+      acc += ri * ri;
+    }
+  }
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+__global__ void xpby_dev_kernel(long long n, const double* __restrict__ z,
+                                const double* __restrict__ st, double* __restrict__ p) {
+  if (st[kStatus] != 0.0) return;
+  const double beta = st[kBeta];
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    p[i] = __dadd_rn(z[i], __dmul_rn(beta, p[i]));
+}
+}  // namespace
+}  // namespace ddmgnn
+
+extern "C" int ddmgnn_pcg_scalars(int op, double* st, double* hist, void* stream) {
+  if (op < 0 || op > 2) return kValueError;
+  pcg_scalars_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(op, st, hist);
+  return cuda_status(cudaGetLastError());
+}
+
+extern "C" int ddmgnn_axpy2_dev(int64_t n, const double* st, const double* p, const double* q,
+                                double* u, double* r, double* work, double* rr_out,
+                                void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int nb = nblocks(n);
+  axpy2_dev_kernel<<<nb, kT, 0, s>>>(n, st, p, q, u, r, work);
+  sum_partials_kernel<<<1, kT, 0, s>>>(nb, work, rr_out);
+  return cuda_status(cudaGetLastError());
+}
+
+extern "C" int ddmgnn_xpby_dev(int64_t n, const double* z, const double* st, double* p,
+                               void* stream) {
+  if (n <= 0) return 0;
+  xpby_dev_kernel<<<nblocks(n), kT, 0, static_cast<cudaStream_t>(stream)>>>(n, z, st, p);
+  return cuda_status(cudaGetLastError());
+}

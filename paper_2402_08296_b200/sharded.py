@@ -458,9 +458,15 @@ class ShardedDdmGnn:
         return full
 
     # -- Krylov -----------------------------------------------------------------------------
-    def pcg(self, b_global, tol: float, max_iter: int):
+    def pcg(self, b_global, tol: float, max_iter: int, check_every: int = 8):
         """Distributed PCG (sparse.py:76-127) with this preconditioner; collective.
-        Returns (u_global, SolveReport) on every rank."""
+        Returns (u_global, SolveReport) on every rank.
+
+        The recurrence's scalars live on the device (``st``, see ddmgnn_pcg_scalars):
+        <p, Ap>, ||r||^2 and <r, z> are reduced into it in place by the all-reduces,
+        alpha / beta / the stopping test are computed there, and the updates turn into
+        no-ops once the solve has stopped — so the host only polls the status every
+        ``check_every`` iterations instead of synchronising on every dot product."""
         import torch
 
         if tol <= 0:
@@ -474,47 +480,56 @@ class ShardedDdmGnn:
         u = torch.zeros_like(bo)
         r = bo.clone()
         q = torch.empty_like(bo)
+        st = torch.zeros(11, dtype=torch.float64, device=self.device)
+        hist = torch.zeros(max_iter + 1, dtype=torch.float64, device=self.device)
+        stream = self._stream
         self._dot(bo, bo, 0)
         nb = float(np.sqrt(self._allreduce_scalar(0)))
         if nb == 0.0:  # sparse.py:93-94
             return np.zeros(self.n), SolveReport(0, [0.0], True, 0.0, tol)
-        history = [1.0]  # r0 = b
         z = self.apply_owned(r)
         pv = z.clone()
-        self._dot(r, z, 0)
-        rho = self._allreduce_scalar(0)
-        it = 0
-        converged = False
-        while it < max_iter:
+        self._c(lib.ddmgnn_dot(n_own, r.data_ptr(), z.data_ptr(), self.work.data_ptr(),
+                               st[0:].data_ptr(), stream()))
+        self.comm.allreduce_(st[0:1])  # rho = <r0, z0>
+        st[4], st[5], st[10] = nb, float(tol), float(max_iter)
+        hist[0] = 1.0  # r0 = b
+        status = 0.0
+        for it in range(max_iter):
             self._halo(pv, self.p_ext)
-            self.ctx.spmv_device(self.p_ext.data_ptr(), self.q_ext.data_ptr(), self._stream())
+            s = stream()
+            self.ctx.spmv_device(self.p_ext.data_ptr(), self.q_ext.data_ptr(), s)
             self._c(lib.ddmgnn_gather(self.q_ext.data_ptr(), self.own_pos.data_ptr(), n_own,
-                                      q.data_ptr(), self._stream()))
-            self._dot(pv, q, 0)
-            pq = self._allreduce_scalar(0)
-            if pq <= 0.0:
-                raise RuntimeError("matrix not SPD: <p, Ap> <= 0")
-            alpha = rho / pq
-            self._c(lib.ddmgnn_axpy2(n_own, alpha, pv.data_ptr(), q.data_ptr(), u.data_ptr(),
-                                     r.data_ptr(), self.work.data_ptr(),
-                                     self.scal[1:].data_ptr(), self._stream()))
-            it += 1
-            rel = float(np.sqrt(self._allreduce_scalar(1))) / nb
-            if not np.isfinite(rel):
-                raise RuntimeError(f"non-finite residual at iteration {it}")
-            history.append(rel)
-            if rel < tol:
-                converged = True
-                break
-            if it >= max_iter:
-                break
+                                      q.data_ptr(), s))
+            self._c(lib.ddmgnn_dot(n_own, pv.data_ptr(), q.data_ptr(), self.work.data_ptr(),
+                                   st[1:].data_ptr(), s))
+            self.comm.allreduce_(st[1:2])
+            s = stream()
+            self._c(lib.ddmgnn_pcg_scalars(0, st.data_ptr(), hist.data_ptr(), s))
+            self._c(lib.ddmgnn_axpy2_dev(n_own, st.data_ptr(), pv.data_ptr(), q.data_ptr(),
+                                         u.data_ptr(), r.data_ptr(), self.work.data_ptr(),
+                                         st[3:].data_ptr(), s))
+            self.comm.allreduce_(st[3:4])
+            self._c(lib.ddmgnn_pcg_scalars(1, st.data_ptr(), hist.data_ptr(), stream()))
+            if (it + 1) % check_every == 0 or it + 1 == max_iter:
+                status = float(st[9].item())
+                if status != 0.0:
+                    break
             self.apply_owned(r, z)
-            self._dot(r, z, 0)
-            rho_new = self._allreduce_scalar(0)
-            beta = rho_new / rho
-            rho = rho_new
-            self._c(lib.ddmgnn_xpby(n_own, z.data_ptr(), beta, pv.data_ptr(), self._stream()))
-        return self.gather_global(u), SolveReport(it, history, converged, history[-1], tol)
+            self._c(lib.ddmgnn_dot(n_own, r.data_ptr(), z.data_ptr(), self.work.data_ptr(),
+                                   st[6:].data_ptr(), stream()))
+            self.comm.allreduce_(st[6:7])
+            s = stream()
+            self._c(lib.ddmgnn_pcg_scalars(2, st.data_ptr(), hist.data_ptr(), s))
+            self._c(lib.ddmgnn_xpby_dev(n_own, z.data_ptr(), st.data_ptr(), pv.data_ptr(), s))
+        sh = st.cpu().numpy()
+        status, iters = int(sh[9]), int(sh[8])
+        if status == 3:
+            raise RuntimeError("matrix not SPD: <p, Ap> <= 0")
+        if status == 4:
+            raise RuntimeError(f"non-finite residual at iteration {iters}")
+        history = hist[: iters + 1].cpu().numpy().tolist()
+        return self.gather_global(u), SolveReport(iters, history, status == 1, history[-1], tol)
 
     def _allreduce_scalar(self, slot: int) -> float:
         t = self.scal[slot:slot + 1]

@@ -33,3 +33,12 @@ t_pcg = time.perf_counter() - t0
 print(json.dumps({"sharded_apply_ms_world1": 1e3 * t_apply, "pcg_s": t_pcg,
                   "iterations": rep.iterations, "ms_per_iteration": 1e3 * t_pcg / rep.iterations,
                   "converged": rep.converged}))
+# host issue cost of one apply_owned (no synchronisation inside the loop)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(50):
+    sh.apply_owned(r, z)
+t_issue = (time.perf_counter() - t0) / 50
+torch.cuda.synchronize()
+t_total = (time.perf_counter() - t0) / 50
+print(json.dumps({"apply_host_issue_ms": 1e3 * t_issue, "apply_wall_ms": 1e3 * t_total}))
