@@ -189,6 +189,25 @@ def test_flat_path_reports_non_finite_states(ddm):
         p(g["r"])
 
 
+def test_empty_subdomain(ddm):
+    """A subdomain without nodes: skipped by the local solves (its ||r_i|| is 0,
+    hybrid.py:105-107), and the coarse space becomes rank deficient (asm.py:39-40)."""
+    from oracle import ddm_oracle as orc
+
+    g = load_golden("small.npz")
+    a, _b, coords, dec = _dec(ddm, g)
+    subs = list(dec.subdomains) + [np.zeros(0, dtype=np.int64)]
+    dec2 = ddm.finish_decomposition(subs, dec.base_owner, dec.overlap)
+    model = ddm.init_model(3, 4, seed=0)
+    p = ddm.build_ddm_gnn(a, coords, dec2, model, level="one")
+    om = orc.model_from_flat(3, 4, model.alpha, 0, ddm.flat_params(model))
+    ref = orc.OraclePreconditioner(a, coords, subs, om, "one")
+    r = g["r"][0]
+    assert rel_l2(p(r), ref(r)) < TOL
+    with pytest.raises(RuntimeError, match="rank deficient"):
+        ddm.build_ddm_gnn(a, coords, dec2, model, level="two")
+
+
 # ---------------------------------------------------------------- invariants
 
 
