@@ -49,6 +49,8 @@ typedef struct ddmgnn_ctx ddmgnn_ctx;
 #define DDMGNN_PRECOND_NONE 0 /* plain CG (sparse.py:130-132) */
 #define DDMGNN_LEVEL_ONE 1    /* one-level GNN-Schwarz (restatement of hybrid.py:112-136 w/o :117) */
 #define DDMGNN_LEVEL_TWO 2    /* two-level: + Nicolaides coarse correction (hybrid.py:117) */
+#define DDMGNN_ASM_ONE 3      /* DDM-LU comparator: exact local solves (asm.py:84-113, "ddm-lu-1") */
+#define DDMGNN_ASM_TWO 4      /* DDM-LU two-level (cli.py:69-70, "ddm-lu-2") */
 
 const char* ddmgnn_last_error(void);
 int ddmgnn_version(void);
@@ -70,6 +72,11 @@ int ddmgnn_set_model(ddmgnn_ctx* ctx, int k_bar, int d, double alpha, const doub
                      int64_t n_params);
 /* Dense row-major inverse of R0 A R0^T (k x k), fp64 (asm.py:35-41). */
 int ddmgnn_set_coarse_inverse(ddmgnn_ctx* ctx, int64_t k, const double* inverse);
+/* DDM-LU comparator: allocate the device buffer for the K dense local inverses
+ * A_i^-1 (row-major, k_i x k_i, subdomain i at offset off[i] doubles, off[K] total;
+ * requires build) and return its device address for the caller to fill (setup
+ * factorises on the GPU).  Enables levels DDMGNN_ASM_ONE / DDMGNN_ASM_TWO. */
+int ddmgnn_alloc_local_inverses(ddmgnn_ctx* ctx, const int64_t* off, double** dev_out);
 /* Node cap of the reference's batching (hybrid.py:49-68, default 100000).  Results
  * never depend on it; it only selects which error the reference would raise first. */
 int ddmgnn_set_batch_cap(ddmgnn_ctx* ctx, int64_t cap);

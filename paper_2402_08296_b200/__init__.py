@@ -6,6 +6,7 @@ declared in include/ddmgnn_b200.h; this package is the host-side mirror of the
 reference's Python interface for that path.
 """
 
+from .asm import AsmPreconditioner, apply_asm, build_asm
 from .decomp import Decomposition, extend, finish_decomposition, nicolaides, restrict
 from .dss import (DssModel, IterationWeights, Mlp, flat_params, init_model, load_model,
                   param_arrays, param_count, save_model)
@@ -19,5 +20,5 @@ __all__ = [
     "DssModel", "IterationWeights", "Mlp", "init_model", "load_model", "save_model",
     "param_count", "param_arrays", "flat_params",
     "DdmGnnPreconditioner", "build_ddm_gnn", "apply_ddm_gnn", "plan_batches",
-    "SolveReport", "pcg", "cg", "validate_csr",
+    "SolveReport", "pcg", "cg", "validate_csr", "AsmPreconditioner", "build_asm", "apply_asm",
 ]

@@ -21,6 +21,8 @@ LIB_PATH = os.environ.get("DDMGNN_B200_LIB") or os.path.join(_HERE, "libddmgnn_b
 PRECOND_NONE = 0
 LEVEL_ONE = 1
 LEVEL_TWO = 2
+ASM_ONE = 3
+ASM_TWO = 4
 LEGACY_STREAM = 1  # cudaStreamLegacy
 
 _i64 = ctypes.c_int64
@@ -50,6 +52,7 @@ SIGNATURES = [
     ("ddmgnn_set_model", _int, [_ctx, _int, _int, _dbl, _pd, _i64]),
     ("ddmgnn_set_coarse_inverse", _int, [_ctx, _i64, _pd]),
     ("ddmgnn_set_batch_cap", _int, [_ctx, _i64]),
+    ("ddmgnn_alloc_local_inverses", _int, [_ctx, _pi64, ctypes.POINTER(_vp)]),
     ("ddmgnn_build", _int, [_ctx]),
     ("ddmgnn_info", _int, [_ctx, _pi64, _int]),
     ("ddmgnn_export_local_graph", _int, [_ctx, _i64, _pi64, _pi32, _pi32, _pf]),
@@ -172,6 +175,12 @@ class Context:
     def set_coarse_inverse(self, inv):
         m = np.ascontiguousarray(inv, dtype=np.float64)
         check(self._lib.ddmgnn_set_coarse_inverse(self._h, m.shape[0], dptr(m)))
+
+    def alloc_local_inverses(self, off: np.ndarray) -> int:
+        o = np.ascontiguousarray(off, dtype=np.int64)
+        ptr = _vp()
+        check(self._lib.ddmgnn_alloc_local_inverses(self._h, i64ptr(o), ctypes.byref(ptr)))
+        return ptr.value
 
     def set_batch_cap(self, cap):
         check(self._lib.ddmgnn_set_batch_cap(self._h, int(cap)))

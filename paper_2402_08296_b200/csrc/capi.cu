@@ -116,7 +116,11 @@ struct ddmgnn_ctx {
   PcgState* d_st = nullptr;
   PcgState* h_st = nullptr;  // pinned
   double *h_pin_a = nullptr, *h_pin_b = nullptr;  // pinned staging (n doubles each)
-  cudaGraphExec_t graph_exec[3] = {nullptr, nullptr, nullptr};
+  cudaGraphExec_t graph_exec[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  // DDM-LU comparator: dense local inverses (row-major, offsets in doubles)
+  double* d_ainv = nullptr;
+  long long* d_ainv_off = nullptr;
+  bool have_asm = false;
 };
 
 extern "C" const char* ddmgnn_last_error(void) { return g_err.c_str(); }
@@ -175,6 +179,8 @@ static void free_layout(ddmgnn_ctx* c) {
   dfree(c->d_r0r); dfree(c->d_scale); dfree(c->d_zloc); dfree(c->d_y);
   dfree(c->d_bad); dfree(c->d_outbad);
   dfree(c->d_hbuf); dfree(c->d_cbuf); dfree(c->d_qbuf); dfree(c->d_bslices);
+  dfree(c->d_ainv); dfree(c->d_ainv_off);
+  c->have_asm = false;
   c->n_bslices = 0;
   c->built = false;
   free_graphs(c);
@@ -481,6 +487,12 @@ extern "C" int ddmgnn_export_local_graph(ddmgnn_ctx* c, int64_t sub, int64_t* n_
 static int ready(ddmgnn_ctx* c, int level) {
   if (!c) return fail(kValueError, "null context");
   if (level == DDMGNN_PRECOND_NONE) return c->n ? kOk : fail(kStateError, "no matrix set");
+  if (level == DDMGNN_ASM_ONE || level == DDMGNN_ASM_TWO) {
+    if (!c->have_asm) return fail(kStateError, "DDM-LU apply needs alloc_local_inverses");
+    if (level == DDMGNN_ASM_TWO && c->coarse_k != c->K)
+      return fail(kStateError, "two-level apply needs set_coarse_inverse");
+    return kOk;
+  }
   if (level != DDMGNN_LEVEL_ONE && level != DDMGNN_LEVEL_TWO)
     return fail(kValueError, "level must be 1 (one-level) or 2 (two-level)");
   if (!c->built) return fail(kStateError, "build must be called before apply");
@@ -527,15 +539,23 @@ static cudaError_t enqueue_gnn(ddmgnn_ctx* c, const double* r, int* status, cons
 // Full apply: z = M r.  mode 1 = PCG (fused <r,z>, beta).
 static cudaError_t enqueue_apply(ddmgnn_ctx* c, const double* r, double* z, int level,
                                  int* status, const int* skip, int mode, cudaStream_t s) {
-  cudaError_t e = enqueue_gnn(c, r, status, skip, s);
+  const bool asm_ = level == DDMGNN_ASM_ONE || level == DDMGNN_ASM_TWO;
+  const bool two = level == DDMGNN_LEVEL_TWO || level == DDMGNN_ASM_TWO;
+  cudaError_t e;
+  if (asm_) {
+    e = launch_asm_local(c->K, c->lay.k_max, c->lay.sub_ptr, c->lay.idx, c->d_ainv_off,
+                         c->d_ainv, c->lay.pou, r, c->d_zloc, c->d_r0r, c->d_scale, skip, s);
+  } else {
+    e = enqueue_gnn(c, r, status, skip, s);
+  }
   if (e != cudaSuccess) return e;
-  if (level == DDMGNN_LEVEL_TWO) {
+  if (two) {
     e = launch_coarse_gemv(c->K, c->d_cinv, c->d_r0r, c->d_y, skip, s);
     if (e != cudaSuccess) return e;
   }
-  return launch_prolong(c->n, level == DDMGNN_LEVEL_TWO, c->lay.tptr, c->lay.tent, c->lay.pou,
-                        c->d_y, c->d_scale, c->d_zloc, z, r, c->d_partials, c->d_st, mode, skip,
-                        s);
+  return launch_prolong(c->n, (two ? 1 : 0) | (asm_ ? 2 : 0), c->lay.tptr, c->lay.tent,
+                        c->lay.pou, c->d_y, c->d_scale, c->d_zloc, z, r, c->d_partials, c->d_st,
+                        mode, skip, s);
 }
 
 // Reproduce the reference's error precedence (hybrid.py:121-131, dss.py:324-325):
@@ -643,6 +663,25 @@ extern "C" int ddmgnn_launch_gnn_only(ddmgnn_ctx* c, const double* r, void* stre
   if (st) return st;
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(enqueue_gnn(c, r, c->d_status, nullptr, pick(c, stream)));
+  return kOk;
+}
+
+extern "C" int ddmgnn_alloc_local_inverses(ddmgnn_ctx* c, const int64_t* off, double** dev_out) {
+  if (!c || !c->built) return fail(kStateError, "build must be called first");
+  if (!off || !dev_out) return fail(kValueError, "null argument");
+  const auto& sp = c->lay.h_sub_ptr;
+  for (int i = 0; i < c->K; ++i) {
+    const int64_t k = sp[i + 1] - sp[i];
+    if (off[i + 1] - off[i] != k * k) return fail(kValueError, "offsets must hold k_i^2 entries");
+  }
+  CUDA_TRY(cudaSetDevice(c->device));
+  const long long total = off[c->K];
+  CUDA_TRY(dalloc(&c->d_ainv, std::max<long long>(total, 1)));
+  std::vector<long long> o(off, off + c->K + 1);
+  CUDA_TRY(upload(&c->d_ainv_off, o));
+  c->have_asm = true;
+  free_graphs(c);
+  *dev_out = c->d_ainv;
   return kOk;
 }
 

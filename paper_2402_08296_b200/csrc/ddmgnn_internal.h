@@ -163,6 +163,10 @@ constexpr int kRedThreads = 256;
 int reduce_blocks(int n);
 cudaError_t launch_coarse_gemv(int K, const double* inv, const double* x, double* y,
                                const int* skip, cudaStream_t s);
+cudaError_t launch_asm_local(int K, int k_max, const int* sub_ptr, const int* idx,
+                             const long long* off, const double* ainv, const double* pou,
+                             const double* r, double* yloc, double* r0r, double* scale,
+                             const int* skip, cudaStream_t s);
 cudaError_t launch_prolong(int n, int two_level, const int* tptr, const int2* tent,
                            const double* pou, const double* y, const double* scale,
                            const double* zloc, double* z, const double* r, double* partials,

@@ -363,7 +363,71 @@ cudaError_t launch_coarse_gemv(int K, const double* inv, const double* x, double
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ exact local solves
+// DDM-LU comparator (asm.py:84-113, the reference's build_asm / apply_asm): local
+// solves y_i = A_i^-1 r_i with dense inverses factorised once at setup (cuSOLVER),
+// CTA per subdomain: r_i staged in shared memory, warp per row of A_i^-1 (fp64,
+// coalesced row reads — an 8 sum_i k_i^2 byte HBM stream), (R0 r)_i for the coarse
+// right-hand side alongside.
+__global__ void __launch_bounds__(256) asm_local_kernel(const int* __restrict__ sub_ptr,
+                                                        const int* __restrict__ idx,
+                                                        const long long* __restrict__ off,
+                                                        const double* __restrict__ ainv,
+                                                        const double* __restrict__ pou,
+                                                        const double* __restrict__ r,
+                                                        double* __restrict__ yloc,
+                                                        double* __restrict__ r0r,
+                                                        double* __restrict__ scale,
+                                                        const int* skip) {
+  if (skip != nullptr && *skip != kRunning) return;
+  extern __shared__ double rs[];
+  __shared__ double part[8];
+  const int sub = blockIdx.x;
+  const int pos0 = sub_ptr[sub], k = sub_ptr[sub + 1] - pos0;
+  double acc = 0.0;
+  for (int n = threadIdx.x; n < k; n += blockDim.x) {
+    const int g = idx[pos0 + n];
+    const double v = r[g];
+    rs[n] = v;
+    acc = fma(pou[g], v, acc);
+  }
+  acc = warp_sum_d(acc);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (blockDim.x >> 5); ++w) t += part[w];
+    r0r[sub] = t;
+    scale[sub] = 1.0;  // every local solve contributes (asm.py:110-111)
+  }
+  const double* a = ainv + off[sub];
+  const int lane = threadIdx.x & 31;
+  for (int row = threadIdx.x >> 5; row < k; row += blockDim.x >> 5) {
+    const double* ar = a + static_cast<long long>(row) * k;
+    double y = 0.0;
+    for (int m = lane; m < k; m += 32) y = fma(__ldcs(&ar[m]), rs[m], y);
+    y = warp_sum_d(y);
+    if (lane == 0) yloc[pos0 + row] = y;
+  }
+}
+
+cudaError_t launch_asm_local(int K, int k_max, const int* sub_ptr, const int* idx,
+                             const long long* off, const double* ainv, const double* pou,
+                             const double* r, double* yloc, double* r0r, double* scale,
+                             const int* skip, cudaStream_t s) {
+  const size_t smem = sizeof(double) * static_cast<size_t>(k_max);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(asm_local_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+  }
+  asm_local_kernel<<<K, 256, smem, s>>>(sub_ptr, idx, off, ainv, pou, r, yloc, r0r, scale, skip);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ prolongation
+// two_level bit 0: add the coarse correction; bit 1: ASM order (local terms first).
 // mode 0: plain apply.  mode 1: PCG — also <r, z> -> rho', beta (sparse.py:123-125).
 __global__ void __launch_bounds__(kRedThreads) prolong_kernel(
     int n, int two_level, const int* __restrict__ tptr, const int2* __restrict__ tent,
@@ -376,13 +440,24 @@ __global__ void __launch_bounds__(kRedThreads) prolong_kernel(
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const int b = tptr[j], e = tptr[j + 1];
     double acc = 0.0;
-    if (two_level) {  // z = r0.T @ y  (CSC matvec order: ascending subdomain)
-      const double w = pou[j];
-      for (int t = b; t < e; ++t) acc = __dadd_rn(acc, __dmul_rn(w, y[tent[t].y]));
-    }
-    for (int t = b; t < e; ++t) {  // z[idx_i] += s_i * sol_i, ascending i (hybrid.py:134-135)
-      const int2 pe = tent[t];
-      if (scale[pe.y] != 0.0) acc = __dadd_rn(acc, zloc[pe.x]);
+    if (two_level & 2) {
+      // ASM order (asm.py:108-113): local sum first, coarse correction added last
+      for (int t = b; t < e; ++t) acc = __dadd_rn(acc, zloc[tent[t].x]);
+      if (two_level & 1) {
+        const double w = pou[j];
+        double c = 0.0;
+        for (int t = b; t < e; ++t) c = __dadd_rn(c, __dmul_rn(w, y[tent[t].y]));
+        acc = __dadd_rn(acc, c);
+      }
+    } else {
+      if (two_level) {  // z = r0.T @ y  (CSC matvec order: ascending subdomain)
+        const double w = pou[j];
+        for (int t = b; t < e; ++t) acc = __dadd_rn(acc, __dmul_rn(w, y[tent[t].y]));
+      }
+      for (int t = b; t < e; ++t) {  // z[idx_i] += s_i * sol_i, ascending i (hybrid.py:134-135)
+        const int2 pe = tent[t];
+        if (scale[pe.y] != 0.0) acc = __dadd_rn(acc, zloc[pe.x]);
+      }
     }
     z[j] = acc;
     if (mode == 1) rz += r[j] * acc;

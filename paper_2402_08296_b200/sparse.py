@@ -102,7 +102,10 @@ def pcg(a, b, precond, tol: float, max_iter: int, u0=None):
         if u0.shape != (n,):
             raise ValueError("u0 dimension mismatch")
     a = _as_csr(a)
-    if isinstance(precond, DdmGnnPreconditioner) and _same_matrix(precond.a, a):
+    from .asm import AsmPreconditioner
+
+    if isinstance(precond, (DdmGnnPreconditioner, AsmPreconditioner)) and \
+            _same_matrix(precond.a, a):
         ctx, level = precond.context, precond._level_code
         u, it, hist, conv = ctx.pcg(b, u0, tol, max_iter, level)
     elif precond is None:
