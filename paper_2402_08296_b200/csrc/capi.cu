@@ -98,7 +98,7 @@ struct ddmgnn_ctx {
   float* d_bank = nullptr;
   int n_big = 0;          // subdomains whose node state does not fit shared memory
   size_t gnn_smem = 0;
-  int cap0 = 0, cap1 = 0;
+  int cap0 = 0;
   // coarse
   int coarse_k = 0;
   double* d_cinv = nullptr;
@@ -357,7 +357,7 @@ extern "C" int ddmgnn_set_coarse_inverse(ddmgnn_ctx* c, int64_t k, const double*
 static int refresh_classes(ddmgnn_ctx* c) {
   if (!c->built || !c->have_model) return kOk;
   const int d = c->model.d;
-  c->gnn_smem = gnn_plan_smem(d, c->lay.k_max, &c->cap0, &c->cap1);
+  c->gnn_smem = gnn_plan_smem(d, c->lay.k_max, &c->cap0);
   const auto& sp = c->lay.h_sub_ptr;
   // oversized subdomains (k > cap0) lead the LPT order; they take the flat path
   int nb = 0;
@@ -525,7 +525,6 @@ static cudaError_t enqueue_gnn(ddmgnn_ctx* c, const double* r, int* status, cons
     a.nl = std::min(M.lmax, M.k_bar - ch * M.lmax);
     a.order_begin = 0;
     a.cap0 = c->cap0;
-    a.cap1 = c->cap1;
     const int k_small = c->n_big < c->K ? c->lay.h_sub_ptr[c->lay.h_order[c->n_big] + 1] -
                                               c->lay.h_sub_ptr[c->lay.h_order[c->n_big]]
                                         : 0;

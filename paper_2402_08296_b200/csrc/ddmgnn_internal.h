@@ -136,7 +136,7 @@ struct GnnArgs {
   int nl;            // layers in this chunk
   int first, last;   // chunk flags
   int order_begin;   // CTA b handles subdomain order[order_begin + b]
-  int cap0, cap1;    // per-CTA node-state placement thresholds (gnn_plan_smem)
+  int cap0;          // largest subdomain of the shared-memory CTA path (gnn_plan_smem)
   const int2* bslices;  // flat path: (subdomain, slice) of every slice of a big subdomain
   int n_bslices;
 };
@@ -145,7 +145,7 @@ int gnn_smem_max_nodes(int d);
 int gnn_bank_offsets(int d, int* o);
 cudaError_t gnn_configure_device();
 cudaError_t upload_bank(int d, const float* dev_bank, cudaStream_t s);  // D2D into the constant bank
-size_t gnn_plan_smem(int d, int k_max, int* cap0, int* cap1);
+size_t gnn_plan_smem(int d, int k_max, int* cap0);
 cudaError_t launch_gnn(int d, int n_ctas, int n_big, int k_max_small, size_t smem,
                        const GnnArgs& a, cudaStream_t s, cudaStream_t side, cudaEvent_t fork,
                        cudaEvent_t join);

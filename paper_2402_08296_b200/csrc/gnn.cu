@@ -92,26 +92,14 @@ cudaError_t upload_bank(int d, const float* dev_bank, cudaStream_t s) {
   }
 }
 
-// Shared-memory plan for a launch whose largest subdomain has k_max nodes:
-// returns the dynamic smem bytes and the per-CTA mode thresholds cap0/cap1.
-size_t gnn_plan_smem(int d, int k_max, int* cap0, int* cap1) {
-  const int node0 = gnn_smem_node_bytes(d);            // h + Q + c
-  int qs = 0;
-  switch (d) {
-#define X(DD) case DD: qs = Cfg<DD>::QS; break;
-    DDM_GNN_DIMS(X)
-#undef X
-    default: break;
-  }
-  const int node1 = 4 * qs;                            // Q only
-  // +1 node: the dummy Q row addressed by SELL padding records
+// Shared-memory plan of the CTA path for subdomains of up to k_max nodes: returns
+// the dynamic smem bytes; *cap0 = the largest k whose node state (Q and h rows
+// 0..k incl. the dummy rows, c) fits — larger subdomains take the flat path.
+size_t gnn_plan_smem(int d, int k_max, int* cap0) {
+  const int node0 = gnn_smem_node_bytes(d);  // h + Q + c
   const size_t m0 = static_cast<size_t>(k_max + 1) * node0 + kTcSmemBytes;
-  const size_t m1 = static_cast<size_t>(k_max + 1) * node1;
-  size_t smem;
-  if (m0 <= static_cast<size_t>(kGnnSmemMax)) smem = m0;
-  else smem = kGnnSmemMax;
+  const size_t smem = m0 <= static_cast<size_t>(kGnnSmemMax) ? m0 : kGnnSmemMax;
   *cap0 = node0 ? static_cast<int>((smem - kTcSmemBytes) / node0) - 1 : 0;
-  *cap1 = node1 ? static_cast<int>(m1 / node1) - 1 : 0;
   // restriction scratch (k doubles) aliases Q: guaranteed since QS >= 2
   return smem;
 }
