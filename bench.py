@@ -59,6 +59,8 @@ def parse():
                     help="weights of the time-to-solution leg (trained; random weights do not "
                          "converge, SURVEY.md finding 4)")
     ap.add_argument("--pcg-max-iter", type=int, default=1000)
+    ap.add_argument("--exchange", default="collective", choices=["collective", "p2p"],
+                    help="multi-GPU halo/term exchange: NCCL all-to-all or peer-memory puts")
     return ap.parse_args()
 
 
@@ -460,7 +462,8 @@ def run_sharded(args, world, rank, local):
     prob, t_setup = build_workload(args)
     model = load_model(args)
     t0 = time.perf_counter()
-    sh = ShardedDdmGnn(prob.system.a, prob.coords, prob.dec, model, level=args.level, device=local)
+    sh = ShardedDdmGnn(prob.system.a, prob.coords, prob.dec, model, level=args.level, device=local,
+                       exchange=args.exchange)
     t_build = time.perf_counter() - t0
     r_glob = np.random.default_rng(0).standard_normal(prob.system.n)
     r = sh.owned_part(r_glob)
@@ -499,7 +502,7 @@ def run_sharded(args, world, rank, local):
     pcg = None
     if not args.no_pcg:
         sh2 = ShardedDdmGnn(prob.system.a, prob.coords, prob.dec, ddm.load_model(args.pcg_weights),
-                            level=args.level, device=local, plans=None)
+                            level=args.level, device=local, exchange=args.exchange)
         dist.barrier()
         t0 = time.perf_counter()
         u, rep = sh2.pcg(prob.system.b, 1e-6, args.pcg_max_iter)

@@ -42,7 +42,7 @@ from .decomp import Decomposition
 from .dss import DssModel, flat_params
 from .sparse import SolveReport
 
-__all__ = ["group_subdomains", "ShardPlan", "plan_shards", "Comm", "ShardedDdmGnn"]
+__all__ = ["group_subdomains", "ShardPlan", "plan_shards", "Comm", "PeerExchange", "ShardedDdmGnn"]
 
 
 # ---------------------------------------------------------------------------- planning
@@ -262,6 +262,10 @@ class Comm:
             out.copy_(torch.cat(parts))
         return out
 
+    def barrier(self):
+        if self.size > 1:
+            self._dist.barrier(group=self.group)
+
     def alltoallv(self, recv, send, recv_counts, send_counts):
         if self.size == 1:
             return recv
@@ -275,6 +279,53 @@ class Comm:
         return recv
 
 
+class PeerExchange:
+    """One-sided exchange over peer memory: every rank maps the other ranks'
+    receive buffers (CUDA IPC handles, all-gathered once) and its gather kernel
+    writes its segment straight into them — over NVLink between the GPUs of one box
+    (P2P), or within one device when several ranks share a GPU (the tests).  The
+    receive layout is the all-to-all one (segments ordered by source rank), so a
+    plan serves both exchange modes.  Ordering: a barrier before the puts (the
+    peers finished reading the previous contents) and after them (the data landed)."""
+
+    def __init__(self, comm: "Comm", recv_buf, recv_counts, send_counts):
+        import torch
+        import torch.distributed as dist
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        self.comm = comm
+        self.send_counts = list(send_counts)
+        me, size = comm.rank, comm.size
+        everyone = [None] * size
+        dist.all_gather_object(everyone, (list(recv_counts), reduce_tensor(recv_buf)),
+                               group=comm.group)
+        self.peers = {}
+        for h, (counts, (fn, args)) in enumerate(everyone):
+            if h == me or self.send_counts[h] == 0:
+                continue
+            buf = fn(*args)  # the peer's receive buffer, mapped into this process
+            self.peers[h] = (buf, int(sum(counts[:me])))
+        self._keep = recv_buf
+
+    def put(self, lib, src_ptr: int, idx, stream: int):
+        """Send segment h of the gather src[idx] into peer h's receive buffer."""
+        self._sync()
+        off = 0
+        for h, cnt in enumerate(self.send_counts):
+            if cnt and h in self.peers:
+                buf, dst = self.peers[h]
+                _lib.check(lib.ddmgnn_gather(src_ptr, idx.data_ptr() + 4 * off, cnt,
+                                             buf.data_ptr() + 8 * dst, stream))
+            off += cnt
+        self._sync()
+
+    def _sync(self):
+        import torch
+
+        torch.cuda.current_stream().synchronize()
+        self.comm.barrier()
+
+
 # ---------------------------------------------------------------------------- rank object
 
 
@@ -283,7 +334,8 @@ class ShardedDdmGnn:
 
     def __init__(self, a: sp.csr_matrix, coords: np.ndarray, dec: Decomposition,
                  model: DssModel, level: str = "two", device: int | None = None, group=None,
-                 plans: list | None = None, batch_nodes_cap: int = 100_000):
+                 plans: list | None = None, batch_nodes_cap: int = 100_000,
+                 exchange: str = "collective"):
         import torch
 
         if level not in ("one", "two"):
@@ -354,6 +406,15 @@ class ShardedDdmGnn:
         self.work = torch.zeros(1184, **f64)
         self.scal = torch.zeros(4, **f64)
         self._all_owned = [pl.owned for pl in plans]
+        if exchange not in ("collective", "p2p"):
+            raise ValueError(f"exchange must be 'collective' or 'p2p', got {exchange!r}")
+        self.exchange = exchange
+        self._p2p_halo = self._p2p_terms = None
+        if exchange == "p2p" and self.comm.size > 1:
+            self._p2p_halo = PeerExchange(self.comm, self.halo_recv, plan.halo_recv_counts,
+                                          plan.halo_send_counts)
+            self._p2p_terms = PeerExchange(self.comm, self.zloc_ext[plan.v_own:],
+                                           plan.term_recv_counts, plan.term_send_counts)
 
     def launches_per_apply(self) -> int:
         """Kernels of libddmgnn_b200 launched by one apply_owned."""
@@ -378,11 +439,14 @@ class ShardedDdmGnn:
                                    ext_vec.data_ptr(), s))
         if self.comm.size == 1:
             return ext_vec
-        self._c(lib.ddmgnn_gather(own_vec.data_ptr(), self.halo_send_idx.data_ptr(),
-                                  p.halo_send_idx.size, self.halo_send.data_ptr(), s))
         ns, nr = p.halo_send_idx.size, p.halo_recv_pos.size
-        self.comm.alltoallv(self.halo_recv[:nr], self.halo_send[:ns], p.halo_recv_counts,
-                            p.halo_send_counts)
+        if self._p2p_halo is not None:
+            self._p2p_halo.put(lib, own_vec.data_ptr(), self.halo_send_idx, s)
+        else:
+            self._c(lib.ddmgnn_gather(own_vec.data_ptr(), self.halo_send_idx.data_ptr(), ns,
+                                      self.halo_send.data_ptr(), s))
+            self.comm.alltoallv(self.halo_recv[:nr], self.halo_send[:ns], p.halo_recv_counts,
+                                p.halo_send_counts)
         self._c(lib.ddmgnn_scatter(self.halo_recv.data_ptr(), self.halo_recv_pos.data_ptr(), nr,
                                    ext_vec.data_ptr(), self._stream()))
         return ext_vec
@@ -422,7 +486,9 @@ class ShardedDdmGnn:
                                           self.y.data_ptr(), s))
         # own terms + remote terms (owner glues in ascending subdomain order)
         self.zloc_ext[:p.v_own].copy_(_view_f64(zloc, p.v_own, self.device))
-        if self.comm.size > 1:
+        if self._p2p_terms is not None:
+            self._p2p_terms.put(lib, zloc, self.term_send_pos, s)
+        elif self.comm.size > 1:
             ns = p.term_send_pos.size
             self._c(lib.ddmgnn_gather(zloc, self.term_send_pos.data_ptr(), ns,
                                       self.term_send.data_ptr(), s))

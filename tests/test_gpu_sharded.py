@@ -39,12 +39,17 @@ def _worker(rank, world, port, q):
         model = ddm.load_model(os.path.join(GOLDEN, "desk_k10_d10.dss"))
         out = {}
         for level in ("two", "one"):
-            sh = ShardedDdmGnn(a, coords, dec, model, level=level)
             ref = ddm.build_ddm_gnn(a, coords, dec, model, level=level)
             r = g["r"]
             z_ref = ref(r)
-            z = sh.gather_global(sh.apply_owned(sh.owned_part(r)))
-            out[f"apply_{level}_maxdiff"] = float(np.max(np.abs(z - z_ref)))
+            for exch in ("collective", "p2p"):
+                sh = ShardedDdmGnn(a, coords, dec, model, level=level, exchange=exch)
+                z = sh.gather_global(sh.apply_owned(sh.owned_part(r)))
+                key = f"apply_{level}_maxdiff" + ("" if exch == "collective" else "_p2p")
+                out[key] = float(np.max(np.abs(z - z_ref)))
+        sh = ShardedDdmGnn(a, coords, dec, model, level="two", exchange="p2p")
+        u, rep = sh.pcg(b, 1e-6, 500)
+        out["p2p_iters"] = rep.iterations
         sh = ShardedDdmGnn(a, coords, dec, model, level="two")
         u, rep = sh.pcg(b, 1e-6, 500)
         res = np.linalg.norm(b - a @ u) / np.linalg.norm(b)
@@ -77,6 +82,8 @@ def test_sharded_apply_and_pcg_match_single_gpu(world):
         assert "error" not in out, (rank, out)
         assert out["apply_two_maxdiff"] == 0.0, out
         assert out["apply_one_maxdiff"] == 0.0, out
+        assert out["apply_two_maxdiff_p2p"] == 0.0 and out["apply_one_maxdiff_p2p"] == 0.0, out
+        assert abs(out["p2p_iters"] - ref_iters) <= 1, out
         assert out["converged"] and abs(out["iters"] - ref_iters) <= 1, (out, ref_iters)
         assert out["relres"] < 1.01e-6
         assert out["hist_len"] == out["iters"] + 1
