@@ -274,10 +274,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        # DDMGNN_BENCH_BACKEND=gloo runs the sharded path with several ranks per GPU
+        # (host-staged collectives) — a functional check on a one-GPU box
+        backend = os.environ.get("DDMGNN_BENCH_BACKEND", "nccl")
+        local = local % max(1, torch.cuda.device_count())
+        torch.cuda.set_device(local)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
         return run_sharded(args, world, rank, local)
+    torch.cuda.set_device(local)
 
     import paper_2402_08296_b200 as ddm
 
