@@ -51,6 +51,7 @@ typedef struct ddmgnn_ctx ddmgnn_ctx;
 #define DDMGNN_LEVEL_TWO 2    /* two-level: + Nicolaides coarse correction (hybrid.py:117) */
 #define DDMGNN_ASM_ONE 3      /* DDM-LU comparator: exact local solves (asm.py:84-113, "ddm-lu-1") */
 #define DDMGNN_ASM_TWO 4      /* DDM-LU two-level (cli.py:69-70, "ddm-lu-2") */
+#define DDMGNN_IC0 5          /* IC(0) comparator (sparse.py:170-227, "ic0") */
 
 const char* ddmgnn_last_error(void);
 int ddmgnn_version(void);
@@ -77,6 +78,13 @@ int ddmgnn_set_coarse_inverse(ddmgnn_ctx* ctx, int64_t k, const double* inverse)
  * requires build) and return its device address for the caller to fill (setup
  * factorises on the GPU).  Enables levels DDMGNN_ASM_ONE / DDMGNN_ASM_TWO. */
 int ddmgnn_alloc_local_inverses(ddmgnn_ctx* ctx, const int64_t* off, double** dev_out);
+/* IC(0) comparator: factorise the context's matrix (zero fill on the lower pattern,
+ * sparse.py:184-227; RuntimeError "IC(0) breakdown: ..." like the reference) and
+ * enable level DDMGNN_IC0 (z = L^-T L^-1 r, sync-free triangular solves). */
+int ddmgnn_set_ic0(ddmgnn_ctx* ctx);
+/* The IC(0) factor L (CSR, lower, diagonal last per row); NULL buffers query nnz. */
+int ddmgnn_export_ic0(ddmgnn_ctx* ctx, int64_t* nnz, int32_t* indptr, int32_t* indices,
+                      double* data);
 /* Node cap of the reference's batching (hybrid.py:49-68, default 100000).  Results
  * never depend on it; it only selects which error the reference would raise first. */
 int ddmgnn_set_batch_cap(ddmgnn_ctx* ctx, int64_t cap);

@@ -23,6 +23,7 @@ LEVEL_ONE = 1
 LEVEL_TWO = 2
 ASM_ONE = 3
 ASM_TWO = 4
+IC0 = 5
 LEGACY_STREAM = 1  # cudaStreamLegacy
 
 _i64 = ctypes.c_int64
@@ -53,6 +54,8 @@ SIGNATURES = [
     ("ddmgnn_set_coarse_inverse", _int, [_ctx, _i64, _pd]),
     ("ddmgnn_set_batch_cap", _int, [_ctx, _i64]),
     ("ddmgnn_alloc_local_inverses", _int, [_ctx, _pi64, ctypes.POINTER(_vp)]),
+    ("ddmgnn_set_ic0", _int, [_ctx]),
+    ("ddmgnn_export_ic0", _int, [_ctx, _pi64, _pi32, _pi32, _pd]),
     ("ddmgnn_build", _int, [_ctx]),
     ("ddmgnn_info", _int, [_ctx, _pi64, _int]),
     ("ddmgnn_export_local_graph", _int, [_ctx, _i64, _pi64, _pi32, _pi32, _pf]),
@@ -181,6 +184,20 @@ class Context:
         ptr = _vp()
         check(self._lib.ddmgnn_alloc_local_inverses(self._h, i64ptr(o), ctypes.byref(ptr)))
         return ptr.value
+
+    def set_ic0(self):
+        check(self._lib.ddmgnn_set_ic0(self._h))
+
+    def export_ic0(self):
+        nnz = ctypes.c_int64(0)
+        check(self._lib.ddmgnn_export_ic0(self._h, ctypes.byref(nnz), None, None, None))
+        n = self.info()["n"]
+        ip = np.zeros(n + 1, dtype=np.int32)
+        ix = np.zeros(max(1, nnz.value), dtype=np.int32)
+        dv = np.zeros(max(1, nnz.value), dtype=np.float64)
+        check(self._lib.ddmgnn_export_ic0(self._h, ctypes.byref(nnz), i32ptr(ip), i32ptr(ix),
+                                          dptr(dv)))
+        return ip, ix[: nnz.value], dv[: nnz.value]
 
     def set_batch_cap(self, cap):
         check(self._lib.ddmgnn_set_batch_cap(self._h, int(cap)))

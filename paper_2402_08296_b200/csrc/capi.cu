@@ -116,11 +116,17 @@ struct ddmgnn_ctx {
   PcgState* d_st = nullptr;
   PcgState* h_st = nullptr;  // pinned
   double *h_pin_a = nullptr, *h_pin_b = nullptr;  // pinned staging (n doubles each)
-  cudaGraphExec_t graph_exec[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  cudaGraphExec_t graph_exec[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   // DDM-LU comparator: dense local inverses (row-major, offsets in doubles)
   double* d_ainv = nullptr;
   long long* d_ainv_off = nullptr;
   bool have_asm = false;
+  // IC(0) comparator: L (lower, diag last) and U = L^T (upper, diag first) in CSR
+  int *d_ic_lp = nullptr, *d_ic_lc = nullptr, *d_ic_up = nullptr, *d_ic_uc = nullptr;
+  double *d_ic_lv = nullptr, *d_ic_uv = nullptr, *d_ic_tmp = nullptr;
+  int *d_ic_ready = nullptr, *d_ic_state = nullptr;
+  Ic0Device ic0;
+  bool have_ic0 = false;
 };
 
 extern "C" const char* ddmgnn_last_error(void) { return g_err.c_str(); }
@@ -192,6 +198,9 @@ extern "C" void ddmgnn_destroy(ddmgnn_ctx* c) {
   cudaStreamSynchronize(c->stream);
   free_layout(c);
   dfree(c->d_rowptr); dfree(c->d_col); dfree(c->d_val);
+  dfree(c->d_ic_lp); dfree(c->d_ic_lc); dfree(c->d_ic_up); dfree(c->d_ic_uc);
+  dfree(c->d_ic_lv); dfree(c->d_ic_uv); dfree(c->d_ic_tmp); dfree(c->d_ic_ready);
+  dfree(c->d_ic_state);
   dfree(c->d_sell_off); dfree(c->d_sell_col); dfree(c->d_sell_val);
   dfree(c->d_bank); dfree(c->d_cinv); dfree(c->d_status);
   dfree(c->d_rin); dfree(c->d_zout);
@@ -487,6 +496,7 @@ extern "C" int ddmgnn_export_local_graph(ddmgnn_ctx* c, int64_t sub, int64_t* n_
 static int ready(ddmgnn_ctx* c, int level) {
   if (!c) return fail(kValueError, "null context");
   if (level == DDMGNN_PRECOND_NONE) return c->n ? kOk : fail(kStateError, "no matrix set");
+  if (level == DDMGNN_IC0) return c->have_ic0 ? kOk : fail(kStateError, "IC(0) apply needs set_ic0");
   if (level == DDMGNN_ASM_ONE || level == DDMGNN_ASM_TWO) {
     if (!c->have_asm) return fail(kStateError, "DDM-LU apply needs alloc_local_inverses");
     if (level == DDMGNN_ASM_TWO && c->coarse_k != c->K)
@@ -541,6 +551,11 @@ static cudaError_t enqueue_apply(ddmgnn_ctx* c, const double* r, double* z, int 
   const bool asm_ = level == DDMGNN_ASM_ONE || level == DDMGNN_ASM_TWO;
   const bool two = level == DDMGNN_LEVEL_TWO || level == DDMGNN_ASM_TWO;
   cudaError_t e;
+  if (level == DDMGNN_IC0) {  // z = L^-T (L^-1 r)  (sparse.py:177-179)
+    e = launch_ic0_apply(c->ic0, r, c->d_ic_tmp, z, skip, s);
+    if (e != cudaSuccess || mode != 1) return e;
+    return launch_rz_beta(c->n, r, z, c->d_partials, c->d_st, s);
+  }
   if (asm_) {
     e = launch_asm_local(c->K, c->lay.k_max, c->lay.sub_ptr, c->lay.idx, c->d_ainv_off,
                          c->d_ainv, c->lay.pou, r, c->d_zloc, c->d_r0r, c->d_scale, skip, s);
@@ -662,6 +677,68 @@ extern "C" int ddmgnn_launch_gnn_only(ddmgnn_ctx* c, const double* r, void* stre
   if (st) return st;
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(enqueue_gnn(c, r, c->d_status, nullptr, pick(c, stream)));
+  return kOk;
+}
+
+extern "C" int ddmgnn_set_ic0(ddmgnn_ctx* c) {
+  if (!c || !c->n) return fail(kStateError, "no matrix set");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const int n = c->n;
+  std::vector<int> rp(n + 1), ci(std::max<long long>(c->nnz, 1));
+  std::vector<double> v(std::max<long long>(c->nnz, 1));
+  CUDA_TRY(cudaMemcpy(rp.data(), c->d_rowptr, sizeof(int) * (n + 1), cudaMemcpyDeviceToHost));
+  if (c->nnz) {
+    CUDA_TRY(cudaMemcpy(ci.data(), c->d_col, sizeof(int) * c->nnz, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(v.data(), c->d_val, sizeof(double) * c->nnz, cudaMemcpyDeviceToHost));
+  }
+  std::vector<int> lp, lc;
+  std::vector<double> lv;
+  std::string err;
+  const int st = ic0_factor(n, rp.data(), ci.data(), v.data(), &lp, &lc, &lv, &err);
+  if (st) return fail(st, err);
+  // U = L^T: row j of U = column j of L, diagonal first (rows of L ascending)
+  const int nnz = lp[n];
+  std::vector<int> up(n + 1, 0), uc(nnz);
+  std::vector<double> uv(nnz);
+  for (int t = 0; t < nnz; ++t) up[lc[t] + 1]++;
+  for (int j = 0; j < n; ++j) up[j + 1] += up[j];
+  {
+    std::vector<int> cur(up.begin(), up.end() - 1);
+    for (int i = 0; i < n; ++i)
+      for (int t = lp[i]; t < lp[i + 1]; ++t) {
+        const int slot = cur[lc[t]]++;
+        uc[slot] = i;
+        uv[slot] = lv[t];
+      }
+  }
+  CUDA_TRY(upload(&c->d_ic_lp, lp)); CUDA_TRY(upload(&c->d_ic_lc, lc));
+  CUDA_TRY(upload(&c->d_ic_lv, lv)); CUDA_TRY(upload(&c->d_ic_up, up));
+  CUDA_TRY(upload(&c->d_ic_uc, uc)); CUDA_TRY(upload(&c->d_ic_uv, uv));
+  CUDA_TRY(dalloc(&c->d_ic_tmp, n));
+  CUDA_TRY(dalloc(&c->d_ic_ready, 2 * n));
+  CUDA_TRY(cudaMemset(c->d_ic_ready, 0, sizeof(int) * 2 * n));
+  CUDA_TRY(dalloc(&c->d_ic_state, 4));
+  CUDA_TRY(cudaMemset(c->d_ic_state, 0, sizeof(int) * 4));
+  Ic0Device& f = c->ic0;
+  f.n = n;
+  f.lp = c->d_ic_lp; f.lc = c->d_ic_lc; f.lv = c->d_ic_lv;
+  f.up = c->d_ic_up; f.uc = c->d_ic_uc; f.uv = c->d_ic_uv;
+  f.ready_l = c->d_ic_ready; f.ready_u = c->d_ic_ready + n; f.state = c->d_ic_state;
+  c->have_ic0 = true;
+  free_graphs(c);
+  return kOk;
+}
+
+extern "C" int ddmgnn_export_ic0(ddmgnn_ctx* c, int64_t* nnz, int32_t* indptr, int32_t* indices,
+                                 double* data) {
+  if (!c || !c->have_ic0) return fail(kStateError, "set_ic0 must be called first");
+  int total = 0;
+  CUDA_TRY(cudaMemcpy(&total, c->d_ic_lp + c->n, sizeof(int), cudaMemcpyDeviceToHost));
+  *nnz = total;
+  if (!indptr) return kOk;
+  CUDA_TRY(cudaMemcpy(indptr, c->d_ic_lp, sizeof(int) * (c->n + 1), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(indices, c->d_ic_lc, sizeof(int) * total, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(data, c->d_ic_lv, sizeof(double) * total, cudaMemcpyDeviceToHost));
   return kOk;
 }
 

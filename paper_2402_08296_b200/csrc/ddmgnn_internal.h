@@ -196,4 +196,16 @@ cudaError_t launch_rz_beta(int n, const double* r, const double* z, double* part
 cudaError_t launch_pcg_init_u0(int n, const double* b, const double* au0, double* r,
                                double* partials, PcgState* st, double* hist, cudaStream_t s);
 
+// ic0.cu — IC(0) comparator
+struct Ic0Device {
+  int n = 0;
+  const int *lp = nullptr, *lc = nullptr, *up = nullptr, *uc = nullptr;
+  const double *lv = nullptr, *uv = nullptr;
+  int *ready_l = nullptr, *ready_u = nullptr, *state = nullptr;
+};
+int ic0_factor(int n, const int* rp, const int* ci, const double* v, std::vector<int>* lp,
+               std::vector<int>* lc, std::vector<double>* lv, std::string* err);
+cudaError_t launch_ic0_apply(const Ic0Device& f, const double* r, double* tmp, double* z,
+                             const int* skip, cudaStream_t s);
+
 }  // namespace ddmgnn

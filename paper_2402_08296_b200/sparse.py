@@ -24,7 +24,7 @@ import scipy.sparse as sp
 
 from . import _lib
 
-__all__ = ["SolveReport", "validate_csr", "pcg", "cg"]
+__all__ = ["SolveReport", "validate_csr", "pcg", "cg", "Ic0Preconditioner", "ic0"]
 
 
 @dataclass
@@ -104,7 +104,7 @@ def pcg(a, b, precond, tol: float, max_iter: int, u0=None):
     a = _as_csr(a)
     from .asm import AsmPreconditioner
 
-    if isinstance(precond, (DdmGnnPreconditioner, AsmPreconditioner)) and \
+    if isinstance(precond, (DdmGnnPreconditioner, AsmPreconditioner, Ic0Preconditioner)) and \
             _same_matrix(precond.a, a):
         ctx, level = precond.context, precond._level_code
         u, it, hist, conv = ctx.pcg(b, u0, tol, max_iter, level)
@@ -119,3 +119,43 @@ def pcg(a, b, precond, tol: float, max_iter: int, u0=None):
 def cg(a, b, tol: float, max_iter: int, u0=None):
     """Unpreconditioned conjugate gradient (sparse.py:130-132)."""
     return pcg(a, b, None, tol, max_iter, u0=u0)
+
+
+class Ic0Preconditioner:
+    """Zero-fill incomplete Cholesky x -> L^-T (L^-1 x) (sparse.py:170-179), on the GPU:
+    factorised once on the host (the reference's algorithm, sparse.py:184-227), applied
+    with two sync-free triangular-solve kernels (csrc/ic0.cu)."""
+
+    def __init__(self, ctx, a):
+        self._ctx = ctx
+        self.a = a
+        self._level_code = _lib.IC0
+
+    @property
+    def context(self):
+        return self._ctx
+
+    @property
+    def l(self) -> sp.csr_matrix:  # noqa: E743 — the reference's attribute name
+        ip, ix, dv = self._ctx.export_ic0()
+        n = ip.size - 1
+        return sp.csr_matrix((dv, ix, ip), shape=(n, n))
+
+    def __call__(self, x):
+        x = np.asarray(x, dtype=float)
+        return self._ctx.apply_host(x, self._level_code)
+
+
+def ic0(a: sp.csr_matrix, device: int = 0) -> Ic0Preconditioner:
+    """Incomplete Cholesky with zero fill on the lower-triangular pattern of A
+    (sparse.py:184-227): RuntimeError("IC(0) breakdown ...") on a missing diagonal or
+    a nonpositive pivot, no diagonal shift."""
+    a = sp.csr_matrix(a)
+    if not a.has_sorted_indices:
+        a = a.copy()
+        a.sort_indices()
+    ctx = _lib.Context(device)
+    ctx.set_matrix(a)
+    ctx.set_ic0()
+    return Ic0Preconditioner(ctx, a)
+

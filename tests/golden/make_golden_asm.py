@@ -42,3 +42,22 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def ic0_fixture():
+    """ic0 factor and PCG-IC(0) history on the A.npz problem (sparse.py:184-227)."""
+    from ddmgnn.sparse import ic0
+
+    g = dict(np.load(os.path.join(HERE, "A.npz")))
+    n = g["b"].shape[0]
+    a = sp.csr_matrix((g["data"], g["indices"], g["indptr"]), shape=(n, n))
+    m = ic0(a)
+    _u, rep = pcg(a, g["b"], m, 1e-6, 5000)
+    l = m.l.tocsr()
+    np.savez_compressed(os.path.join(HERE, "ic0.npz"), l_indptr=l.indptr, l_indices=l.indices,
+                        l_data=l.data, z=m(g["r"]), hist=np.asarray(rep.residual_history))
+    print("ic0", l.nnz, rep.iterations)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "ic0":
+    ic0_fixture()

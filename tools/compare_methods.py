@@ -22,6 +22,7 @@ a, b = prob.system.a, prob.system.b
 desk = ddm.load_model(os.path.join(ROOT, "tests", "golden", "desk_k10_d10.dss"))
 methods = {
     "cg": lambda: None,
+    "ic0": lambda: ddm.ic0(a),
     "ddm-lu-1": lambda: ddm.build_asm(a, prob.dec, "one"),
     "ddm-lu-2": lambda: ddm.build_asm(a, prob.dec, "two"),
     "ddm-gnn": lambda: ddm.build_ddm_gnn(a, prob.coords, prob.dec, desk),
