@@ -235,13 +235,14 @@ def run_reference(args):
 # ----------------------------------------------------------------------------- GPU arm
 
 
-def time_to_solution(ddm, p, prob, args, ctx, lvl, dev, stream):
+def time_to_solution(ddm, p, prob, args, ctx, lvl, dev, stream, weights=None):
     """Device-timed PCG (sparse.py:76-127) to 1e-6 with the pinned trained weights:
     warm-up solve (captures the CUDA graphs), then one solve between CUDA events
     on the solve's stream; setup excluded (as cli.py:195-199 minus the build)."""
     import torch
 
-    model = ddm.load_model(args.pcg_weights)
+    weights = weights or args.pcg_weights
+    model = ddm.load_model(weights)
     p.reload_model(model)
     b = torch.tensor(prob.system.b, device=dev)
     u = torch.empty_like(b)
@@ -263,7 +264,7 @@ def time_to_solution(ddm, p, prob, args, ctx, lvl, dev, stream):
     return {"seconds": sec, "iterations": it, "converged": conv, "final_relres": hist[-1],
             "true_relres": true_rel, "ms_per_iteration": 1e3 * sec / max(1, it),
             "max_iter": args.pcg_max_iter, "tol": 1e-6,
-            "weights": os.path.relpath(args.pcg_weights, ROOT),
+            "weights": os.path.relpath(weights, ROOT),
             "timing": "CUDA events on the solve stream, device-resident b/u, graphs warm"}
 
 
@@ -379,9 +380,15 @@ def run_ours(args):
     e2e_value = world / float(e2e_t.item())
 
     # ---- time-to-solution: device-resident PCG to 1e-6 (trained weights) ----
-    pcg = None
+    pcg = pcg_trained = None
     if not args.no_pcg:
         pcg = time_to_solution(ddm, p, prob, args, ctx, lvl, dev, stream)
+        # weights trained on the GPU for this subdomain size (tools/train_gpu.py), if present
+        for cand in ("gpu_k10_ns1000_long.dss", "gpu_k10_ns1000.dss"):
+            path = os.path.join(ROOT, "weights", cand)
+            if os.path.exists(path) and args.subdomain_size == 1000 and args.kbar == 10:
+                pcg_trained = time_to_solution(ddm, p, prob, args, ctx, lvl, dev, stream, path)
+                break
 
     peaks = {}
     try:
@@ -448,6 +455,7 @@ def run_ours(args):
             "gpu_launches": per_step_launches * args.steps,
             "clocks": clocks,
             "pcg": pcg,
+            "pcg_trained_weights": pcg_trained,
             "setup_s": {"problem_build": t_setup, "preconditioner_build": t_build},
         }
         print(json.dumps(out))
