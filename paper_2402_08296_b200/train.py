@@ -21,7 +21,7 @@ import numpy as np
 import scipy.sparse as sp
 
 from .asm import build_asm, extract_local_matrix
-from .dss import DssModel, flat_params, init_model
+from .dss import DssModel
 from .sparse import pcg
 
 __all__ = ["LocalProblem", "harvest", "Trainer"]
@@ -234,11 +234,3 @@ def _arrays(model: DssModel):
         for mlp in (w.phi_out, w.phi_in, w.psi, w.dec):
             out.extend([mlp.w1, mlp.b1, mlp.w2, mlp.b2])
     return out
-
-
-def new_model(k_bar: int, d: int, seed: int = 1, alpha: float = 1e-3) -> DssModel:
-    return init_model(k_bar, d, alpha=alpha, seed=seed)
-
-
-def _check_flat(model: DssModel) -> np.ndarray:  # pragma: no cover - debugging aid
-    return flat_params(model)
