@@ -420,7 +420,10 @@ class ShardedDdmGnn:
         """Kernels of libddmgnn_b200 launched by one apply_owned."""
         info = self.ctx.info()
         multi = self.comm.size > 1
-        gnn = info["n_chunks"] * (1 + (1 if info["n_big"] else 0))
+        gnn = 0
+        for ch in range(info["n_chunks"]):
+            nl = min(info["lmax"], info["k_bar"] - ch * info["lmax"])
+            gnn += 1 + ((2 * nl + (1 if ch == 0 else 0)) if info["n_big"] else 0)
         return (1 + 2 * multi) + gnn + 4 + (self.kinv is not None) + multi + 1
 
     # -- helpers --------------------------------------------------------------------------
