@@ -168,7 +168,7 @@ class Trainer:
 
     def fit(self, train, val, epochs: int, lr: float = 1e-2, batch_size: int = 100,
             clip_norm: float = 1e-2, factor: float = 0.1, patience: int = 10,
-            min_lr: float = 1e-5, seed: int = 0, log_every: int = 0):
+            min_lr: float = 1e-5, seed: int = 0, log_every: int = 0, on_epoch=None):
         """Adam + global-norm clipping + plateau schedule, as dss.py:392-469."""
         import torch
 
@@ -208,6 +208,8 @@ class Trainer:
             if log_every and epoch % log_every == 0:
                 print(f"epoch {epoch} train {train_loss:.4e} val {val_loss:.4e} lr {lr:g}",
                       flush=True)
+            if on_epoch is not None:  # e.g. solver-aware checkpoint selection
+                on_epoch(epoch, self.to_model)
             if val:
                 if val_loss < best:
                     best, bad = val_loss, 0
