@@ -60,7 +60,7 @@ constexpr int kFlatWarps = 8;        // slices (warps) per CTA of the flat path
 #endif
 // shared memory reserved at the start of the CTA path's dynamic smem for the
 // tensor-core B operand (WQ^T hi/lo, 2 x 32 x 16 fp32)
-constexpr int kTcSmemBytes = GNN_TC_Q ? 4096 : 0;
+constexpr int kTcSmemBytes = GNN_TC_Q == 2 ? 14336 : (GNN_TC_Q ? 4096 : 0);
 constexpr int kGnnSmemMax = 227 * 1024 - 2048;  // dynamic smem cap (static smem < 2 KB)
 
 struct DeviceLayout {

@@ -306,11 +306,18 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ int tc_kmaj(int r, int k) {
   return (r >> 3) * ((kTcK / 4) * 128) + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4;
 }
-__device__ __forceinline__ uint64_t tc_sdesc(uint32_t addr) {
+__device__ __forceinline__ uint64_t tc_sdesc(uint32_t addr, uint32_t sbo = (kTcK / 4) * 128) {
   return static_cast<uint64_t>((addr >> 4) & 0x3FFF) |
          (static_cast<uint64_t>(128 >> 4) << 16) |                     // LBO: next K core
-         (static_cast<uint64_t>(((kTcK / 4) * 128) >> 4) << 32) |      // SBO: next 8 rows
+         (static_cast<uint64_t>(sbo >> 4) << 32) |                     // SBO: next 8 rows
          (static_cast<uint64_t>(1) << 46);                             // sm_100 version
+}
+// K-major SWIZZLE_NONE index for a K-wide operand
+__device__ __forceinline__ int tc_kmaj_k(int r, int k, int kk) {
+  return (r >> 3) * ((kk / 4) * 128) + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4;
+}
+constexpr uint32_t tc_idesc(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(n >> 3) << 17) | (8u << 24);
 }
 constexpr uint32_t kTcIdesc = (1u << 4) | (2u << 7) | (2u << 10) |
                               (static_cast<uint32_t>(kTcN >> 3) << 17) | (8u << 24);
@@ -341,11 +348,12 @@ __device__ __forceinline__ void tc_ld4(uint32_t taddr, float (&v)[4]) {
                : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
                : "r"(taddr));
 }
-__device__ __forceinline__ void tc_mma(uint32_t d, uint32_t a, uint64_t b, int acc) {
+__device__ __forceinline__ void tc_mma(uint32_t d, uint32_t a, uint64_t b, int acc,
+                                       uint32_t idesc = kTcIdesc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %4, p;\n\t}\n"
-      ::"r"(d), "r"(a), "l"(b), "r"(acc), "r"(kTcIdesc));
+      ::"r"(d), "r"(a), "l"(b), "r"(acc), "r"(idesc));
 }
 __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
   asm volatile(
@@ -430,6 +438,256 @@ __device__ __forceinline__ void tc_phase_q(int k, int warp, uint32_t tmem, unsig
 }
 #endif
 
+
+#if GNN_TC_Q == 2
+// ---- the whole layer's node mat-vecs on the tensor cores (GNN_TC_Q == 2) ----------
+// Per layer the CTA stages four B operands (tf32 hi/lo, K-major) in shared memory:
+// WQ^T and WP^T (N=32, K=16), WU^T (N=16, K=32: psi's first layer with the folded
+// message layer), WP2^T (N=16, K=16).  Each 4-warp group owns 96 TMEM columns
+// (A staging 0..63, accumulator 64..95) and walks its 128-node tiles: Q (phase A),
+// then per tile P -> edge loop on the CUDA cores -> psi1 -> psi2 (phase B), each
+// mat-vec a 3xTF32 GEMM issued by one thread after a group barrier and completed
+// through the group's mbarrier.
+constexpr int kTcCols = 96;
+constexpr int kTcB_Q = 0, kTcB_P = 2 * 512, kTcB_U = 4 * 512, kTcB_2 = 6 * 512;  // floats
+
+template <int D, int W>
+__device__ __forceinline__ void tc_stage_all(unsigned char* tc) {
+  using C = Cfg<D>;
+  float* b = reinterpret_cast<float*>(tc);
+  for (int i = threadIdx.x; i < 32 * 16; i += blockDim.x) {  // WQ / WP: N=32, K=16
+    const int n = i / 16, kk = i % 16;
+    const bool in = n < 2 * D && kk < D + 2;
+    const float wq = in ? c_w[W + C::OFF_WQ + kk * C::D2P + n] : 0.f;
+    const float wp = in ? c_w[W + C::OFF_WP + kk * C::D2P + n] : 0.f;
+    const int o = tc_kmaj_k(n, kk, 16) >> 2;
+    float hi = tf32_rna(wq);
+    b[kTcB_Q + o] = hi;
+    b[kTcB_Q + 512 + o] = tf32_rna(wq - hi);
+    hi = tf32_rna(wp);
+    b[kTcB_P + o] = hi;
+    b[kTcB_P + 512 + o] = tf32_rna(wp - hi);
+  }
+  for (int i = threadIdx.x; i < 16 * 32; i += blockDim.x) {  // WU: N=16, K=32
+    const int n = i / 32, kk = i % 32;
+    const float w = (n < D && kk < 3 * D + 2) ? c_w[W + C::OFF_WU + kk * C::DP + n] : 0.f;
+    const int o = tc_kmaj_k(n, kk, 32) >> 2;
+    const float hi = tf32_rna(w);
+    b[kTcB_U + o] = hi;
+    b[kTcB_U + 512 + o] = tf32_rna(w - hi);
+  }
+  for (int i = threadIdx.x; i < 16 * 16; i += blockDim.x) {  // WP2: N=16, K=16
+    const int n = i / 16, kk = i % 16;
+    const float w = (n < D && kk < D) ? c_w[W + C::OFF_WP2 + kk * C::DP + n] : 0.f;
+    const int o = tc_kmaj_k(n, kk, 16) >> 2;
+    const float hi = tf32_rna(w);
+    b[kTcB_2 + o] = hi;
+    b[kTcB_2 + 256 + o] = tf32_rna(w - hi);
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+}
+
+// stage NV values (hi at col a0, lo at col a0 + NV) of this thread's TMEM row
+// The split is hi = x with the 13 low mantissa bits cleared (one LOP3; cvt.rna.tf32
+// is a ~10-instruction sequence here) and lo = x - hi (exact); the tensor core
+// reads lo as tf32 by truncation, an error below 2^-21 |x|.
+template <int NV>
+__device__ __forceinline__ void tc_stage_row(uint32_t row_addr, const float (&v)[NV]) {
+  static_assert(NV % 16 == 0, "16-column groups");
+#pragma unroll
+  for (int g = 0; g < NV / 16; ++g) {
+    float hi[16], lo[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      hi[i] = __uint_as_float(__float_as_uint(v[16 * g + i]) & 0xFFFFE000u);
+      lo[i] = v[16 * g + i] - hi[i];
+    }
+    tc_st16(row_addr + 16 * g, hi);
+    tc_st16(row_addr + NV + 16 * g, lo);
+  }
+}
+
+// group GEMM: D(cols + 64) = A(cols, K = 8 KSTEPS, hi | lo) . B(smem hi | lo)
+template <int KSTEPS, int N>
+__device__ __forceinline__ void tc_group_gemm(int group, int quarter, int lane, uint32_t cols,
+                                              uint32_t b_hi, uint32_t b_lo, uint32_t mb,
+                                              uint32_t& uses) {
+  constexpr uint32_t sbo = KSTEPS * 2 * 128;
+  constexpr uint32_t idesc = tc_idesc(N);
+  asm volatile("tcgen05.wait::st.sync.aligned;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  asm volatile("bar.sync %0, 128;" ::"r"(1 + group));
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (quarter == 0 && lane == 0) {
+    const uint32_t d = cols + 64;
+#pragma unroll
+    for (int ks = 0; ks < KSTEPS; ++ks) {
+      tc_mma(d, cols + 8 * ks, tc_sdesc(b_hi + ks * 256, sbo), ks > 0, idesc);
+      tc_mma(d, cols + 8 * ks, tc_sdesc(b_lo + ks * 256, sbo), 1, idesc);
+      tc_mma(d, cols + 8 * KSTEPS + 8 * ks, tc_sdesc(b_hi + ks * 256, sbo), 1, idesc);
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 ::"r"(mb));
+  }
+  mbar_wait(mb, uses & 1);
+  ++uses;
+  asm volatile("tcgen05.fence::after_thread_sync;");
+}
+
+template <int D, int W>
+__device__ __forceinline__ void tc_layer(const SmemState<D>& ns, int k, int warp,
+                                         const float2* xy, const float2* edges,
+                                         const int* slice_off, const uint16_t* deg, float alpha,
+                                         int* bad, int layer_no, uint32_t tmem, uint64_t* mbar,
+                                         uint32_t& uses) {
+  using C = Cfg<D>;
+  constexpr int NP2 = C::NP2, NPH = C::NPH;
+  static_assert(2 * D <= 32 && D + 2 <= 16 && 3 * D + 2 <= 32, "tile shapes");
+  const int lane = threadIdx.x & 31, quarter = warp & 3, group = warp >> 2;
+  const int ngroups = blockDim.x >> 7;
+  const uint32_t cols = tmem + group * kTcCols;
+  const uint32_t row = cols + (static_cast<uint32_t>(quarter * 32) << 16);
+  const uint32_t bq = smem_u32(ns.tc);
+  const uint32_t mb = smem_u32(&mbar[group]);
+  const int ntiles = (k + 127) >> 7;
+  tc_stage_all<D, W>(ns.tc);
+  __syncthreads();
+  // ---- phase A: Q rows ----
+  for (int t = group; t < ntiles; t += ngroups) {
+    const int nn = min(t * 128 + quarter * 32 + lane, k - 1);
+    float a[16];
+    {
+      float hin[D + 2];
+      load_hxy<D>(ns.h + nn * C::HS, __ldg(xy + nn), hin);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) a[i] = i < D + 2 ? hin[i] : 0.f;
+    }
+    tc_stage_row<16>(row, a);
+    tc_group_gemm<2, 32>(group, quarter, lane, cols, bq + 4 * kTcB_Q, bq + 4 * (kTcB_Q + 512), mb,
+                         uses);
+    float v0[16], v1[4];
+    tc_ld16(row + 64, v0);
+    tc_ld4(row + 80, v1);
+    asm volatile("tcgen05.wait::ld.sync.aligned;");
+    float qs[C::QS];
+#pragma unroll
+    for (int j = 0; j < C::QS; ++j) qs[j] = j < 2 * D ? (j < 16 ? v0[j] : v1[j - 16]) : 0.f;
+    store_vec<C::QS>(ns.q + nn * C::QS, qs);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  // ---- phase B ----
+  int first_bad = 0;
+  for (int t = group; t < ntiles; t += ngroups) {
+    const int n0 = t * 128 + quarter * 32;
+    const int n = n0 + lane, nn = min(n, k - 1);
+    float hv[C::DH];
+    load_vec<C::DH>(ns.h + nn * C::HS, hv);
+    float2 xyn = __ldg(xy + nn);
+    // P = b1 + [h, x, y] . WP
+    float2 p[NP2];
+    {
+      float a[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) a[i] = i < D ? hv[i] : (i == D ? xyn.x : (i == D + 1 ? xyn.y : 0.f));
+      tc_stage_row<16>(row, a);
+      tc_group_gemm<2, 32>(group, quarter, lane, cols, bq + 4 * kTcB_P, bq + 4 * (kTcB_P + 512),
+                           mb, uses);
+      float v0[16], v1[4];
+      tc_ld16(row + 64, v0);
+      tc_ld4(row + 80, v1);
+      asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+      for (int j = 0; j < NP2; ++j) {
+        const float x0 = 2 * j < 16 ? v0[2 * j] : v1[2 * j - 16];
+        const float x1 = 2 * j + 1 < 16 ? v0[2 * j + 1] : v1[2 * j + 1 - 16];
+        p[j] = fadd2(make_float2(x0, x1), cpair(W + C::OFF_B1 + 2 * j));
+      }
+    }
+    // edge aggregation on the CUDA cores (as slice_u)
+    float2 s[NP2];
+#pragma unroll
+    for (int j = 0; j < NP2; ++j) s[j] = make_float2(0.f, 0.f);
+    {
+      const bool live = n0 < k;  // warp-uniform
+      const int so = live ? uni(slice_off[n0 >> 5]) : 0;
+      const int width = live ? (uni(slice_off[(n0 >> 5) + 1]) - so) >> 5 : 0;
+      const float2 dummy = make_float2(0.f, __int_as_float(k));
+      const float2* ep = edges + so + lane;
+      float2 rec = width > 0 ? __ldg(ep) : dummy;
+      for (int e = 0; e < width; ++e) {
+        const float2 cur = rec;
+        rec = e + 1 < width ? __ldg(ep + 32 * (e + 1)) : dummy;
+        float qt[C::QS];
+        load_vec<C::QS>(ns.q + __float_as_int(cur.y) * C::QS, qt);
+        const float2 len = bcast(cur.x);
+#pragma unroll
+        for (int j = 0; j < NP2; ++j) {
+          float2 x = fadd2(p[j], make_float2(qt[2 * j], qt[2 * j + 1]));
+          x = ffma2(len, cpair(W + C::OFF_WL + 2 * j), x);
+          s[j] = fadd2(s[j], relu2x(x));
+        }
+      }
+    }
+    // psi first layer: [h, c, deg, S] . WU
+    float u[16];
+    {
+      float a[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) a[i] = 0.f;
+#pragma unroll
+      for (int i = 0; i < D; ++i) a[i] = hv[i];
+      a[D] = ns.c[nn];
+      a[D + 1] = static_cast<float>(deg[nn]);
+#pragma unroll
+      for (int j = 0; j < NP2; ++j) {
+        a[D + 2 + 2 * j] = s[j].x;
+        a[D + 3 + 2 * j] = s[j].y;
+      }
+      tc_stage_row<32>(row, a);
+      tc_group_gemm<4, 16>(group, quarter, lane, cols, bq + 4 * kTcB_U, bq + 4 * (kTcB_U + 512),
+                           mb, uses);
+      tc_ld16(row + 64, u);
+      asm volatile("tcgen05.wait::ld.sync.aligned;");
+    }
+    // relu (u + bp1) -> psi second layer
+    float o16[16];
+    {
+      float a[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float ui = i < D ? u[i] + c_w[W + C::OFF_BP1 + i] : 0.f;
+        a[i] = ui + fabsf(ui);  // 2 relu, the 1/2 is folded into WP2
+      }
+      tc_stage_row<16>(row, a);
+      tc_group_gemm<2, 16>(group, quarter, lane, cols, bq + 4 * kTcB_2, bq + 4 * (kTcB_2 + 256),
+                           mb, uses);
+      tc_ld16(row + 64, o16);
+      asm volatile("tcgen05.wait::ld.sync.aligned;");
+    }
+    float hn[C::DH];
+    float fin = 0.f;
+#pragma unroll
+    for (int i = 0; i < C::DH; ++i) {
+      if (i < D) {
+        const float o = o16[i] + c_w[W + C::OFF_BP2 + i];
+        hn[i] = fmaf(alpha, o, hv[i]);
+        fin = fmaf(hn[i], 0.f, fin);
+      } else {
+        hn[i] = 0.f;
+      }
+    }
+    if (fin != 0.f && first_bad == 0 && n < k) first_bad = layer_no;
+    store_vec<C::DH>(ns.h + min(n, k) * C::HS, hn);
+    asm volatile("tcgen05.fence::before_thread_sync;");
+  }
+  if (first_bad != 0 && *bad == 0) *bad = first_bad;
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+}
+#endif
+
 // one layer, all slices of the CTA's subdomain (warp w: slices w, w + nwarps, ...)
 template <int D, int W>
 __device__ __forceinline__ void cta_layer(const SmemState<D>& ns, int k, int warp,
@@ -438,7 +696,10 @@ __device__ __forceinline__ void cta_layer(const SmemState<D>& ns, int k, int war
                                           float alpha, int* bad, int layer_no,
                                           uint32_t tmem, uint64_t* mbar, uint32_t& uses) {
   const int step = blockDim.x;
-#if GNN_TC_Q
+#if GNN_TC_Q == 2
+  tc_layer<D, W>(ns, k, warp, xy, edges, slice_off, deg, alpha, bad, layer_no, tmem, mbar, uses);
+  return;
+#elif GNN_TC_Q
   tc_stage_wq<D, W>(ns.tc);
   __syncthreads();
   tc_phase_q<D>(k, warp, tmem, ns.tc, mbar, uses, ns.h, ns.q, xy);
