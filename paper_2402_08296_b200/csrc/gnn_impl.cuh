@@ -243,8 +243,10 @@ __device__ __forceinline__ bool slice_u(int n0, int k, float* h, const float* q,
     hn[2 * j] = hp.x;
     hn[2 * j + 1] = (2 * j + 1 < D) ? hp.y : 0.f;
   }
-  // the lane's own row only (nobody else reads h): in-place update; lanes past k
-  // write the dummy row k
+  // the lane's own row only: in-place update; lanes past k write the dummy row k.
+  // Lanes past k read row k-1 above, so order those reads before the valid lane's
+  // write of row k-1 explicitly (no divergence here, but keep the warp contract)
+  __syncwarp();
   store_vec<C::DH>(h + min(n, k) * C::HS, hn);
   return (fin.x != 0.f || fin.y != 0.f) && n < k;
 }
