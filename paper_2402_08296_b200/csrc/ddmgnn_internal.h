@@ -55,6 +55,9 @@ enum DevStatus : int {
 constexpr int kGnnThreads = GNN_THREADS;  // GNN CTA size (28 warps/SM; measured best of 640-1024)
 constexpr int kConstFloats = 16384;  // 64 KB constant bank
 constexpr int kFlatWarps = 8;        // slices (warps) per CTA of the flat path
+#ifndef GNN_Q2
+#define GNN_Q2 1  // phase A two slices per warp (shared weight loads; 2.4% faster)
+#endif
 #ifndef GNN_TC_Q
 #define GNN_TC_Q 0  // phase-A projection on tcgen05 (3xTF32) instead of FFMA2
 #endif

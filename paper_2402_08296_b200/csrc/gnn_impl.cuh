@@ -156,6 +156,48 @@ __device__ __forceinline__ void slice_q(int n0, int k, const float* h, float* q,
   store_vec<C::QS>(q + nn * C::QS, qs);
 }
 
+// phase A for two slices at once (n0a, n0b): every weight pair loaded once feeds
+// both slices' FFMA2; the outputs are produced in two halves to bound registers.
+template <int D, int W>
+__device__ __forceinline__ void slice_q2(int n0a, int n0b, int k, const float* h, float* q,
+                                         const float2* __restrict__ xy) {
+  using C = Cfg<D>;
+  constexpr int NP2 = C::NP2, H1 = NP2 / 2;
+  const int lane = threadIdx.x & 31;
+  const int na = min(n0a + lane, k - 1), nb = min(n0b + lane, k - 1);
+  float xa[D + 2], xb[D + 2];
+  load_hxy<D>(h + na * C::HS, __ldg(xy + na), xa);
+  load_hxy<D>(h + nb * C::HS, __ldg(xy + nb), xb);
+  float qsa[C::QS], qsb[C::QS];
+#pragma unroll
+  for (int j = 0; j < C::QS; ++j) qsa[j] = qsb[j] = 0.f;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    const int j0 = half ? H1 : 0, j1 = half ? NP2 : H1;
+    float2 aa[NP2 - H1 > H1 ? NP2 - H1 : H1], ab[NP2 - H1 > H1 ? NP2 - H1 : H1];
+#pragma unroll
+    for (int j = 0; j < j1 - j0; ++j) aa[j] = ab[j] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int m = 0; m < D + 2; ++m) {
+#pragma unroll
+      for (int j = j0; j < j1; ++j) {
+        const float2 w = cpair(W + C::OFF_WQ + m * C::D2P + 2 * j);
+        aa[j - j0] = ffma2(bcast(xa[m]), w, aa[j - j0]);
+        ab[j - j0] = ffma2(bcast(xb[m]), w, ab[j - j0]);
+      }
+    }
+#pragma unroll
+    for (int j = j0; j < j1; ++j) {
+      qsa[2 * j] = aa[j - j0].x;
+      qsa[2 * j + 1] = aa[j - j0].y;
+      qsb[2 * j] = ab[j - j0].x;
+      qsb[2 * j + 1] = ab[j - j0].y;
+    }
+  }
+  store_vec<C::QS>(q + na * C::QS, qsa);
+  store_vec<C::QS>(q + nb * C::QS, qsb);
+}
+
 // phase B: edge aggregation + node update; returns whether the lane's node became
 // non-finite and leaves the updated latent in hn (for a fused decoder)
 template <int D, int W>
@@ -706,7 +748,17 @@ __device__ __forceinline__ void cta_layer(const SmemState<D>& ns, int k, int war
   __syncthreads();
   tc_phase_q<D>(k, warp, tmem, ns.tc, mbar, uses, ns.h, ns.q, xy);
 #else
+#if GNN_Q2
+  {  // slice pairs (s, s + nslices/2 rounded): one weight load feeds both
+    const int nsl = (k + 31) >> 5, half = (nsl + 1) >> 1;
+    for (int sa = warp; sa < half; sa += step >> 5) {
+      const int sb = sa + half < nsl ? sa + half : sa;  // odd count: last pair repeats sa
+      slice_q2<D, W>(sa * 32, sb * 32, k, ns.h, ns.q, xy);
+    }
+  }
+#else
   for (int n0 = 32 * warp; n0 < k; n0 += step) slice_q<D, W>(n0, k, ns.h, ns.q, xy);
+#endif
 #endif
   __syncthreads();
   int first_bad = 0;
