@@ -405,12 +405,9 @@ def run_ours(args):
     achieved = flops / (gnn_ms * 1e-3) / 1e12
     gnn_traffic, traffic_src = profiled_traffic("gnn_kernel")
     spmv_traffic, _ = profiled_traffic("spmv_kernel")
-    # per chunk: gnn_kernel, and for oversized subdomains the flat path (prologue in
-    # the first chunk + 2 launches per layer)
-    n_gnn_launches = 0
-    for ch in range(info["n_chunks"]):
-        nl = min(info["lmax"], info["k_bar"] - ch * info["lmax"])
-        n_gnn_launches += 1 + ((2 * nl + (1 if ch == 0 else 0)) if info["n_big"] else 0)
+    # per chunk: gnn_kernel, one launch per cluster size, and for subdomains beyond an
+    # 8-CTA cluster the flat path (prologue in the first chunk + 2 launches per layer)
+    n_gnn_launches = ctx.gnn_launches()
     per_step_launches = n_gnn_launches + (1 if lvl == 2 else 0) + 1
     clocks = clk.summary()
     if rank == 0:

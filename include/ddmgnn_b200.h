@@ -91,7 +91,9 @@ int ddmgnn_set_batch_cap(ddmgnn_ctx* ctx, int64_t cap);
 /* Build the device layout of the per-subdomain graphs (requires matrix, geometry
  * and decomposition). */
 int ddmgnn_build(ddmgnn_ctx* ctx);
-/* out[0..11] = n, K, V, E, E_pad, k_max, slices, k_bar, d, lmax, n_chunks, n_big */
+/* out[0..13] = n, K, V, E, E_pad, k_max, slices, k_bar, d, lmax, n_chunks, n_big,
+ * n_cluster (of the n_big oversized subdomains, those on the cluster path),
+ * cluster_launches (cluster sizes in use: one launch each per chunk) */
 int ddmgnn_info(ddmgnn_ctx* ctx, int64_t* out, int n_out);
 /* Edges of subdomain `sub` as built on the device (for parity tests): src/dst local
  * indices and fp32 {dx, dy, |d|}.  Pass NULL buffers to query the count. */

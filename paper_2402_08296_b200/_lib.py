@@ -205,11 +205,24 @@ class Context:
     def build(self):
         check(self._lib.ddmgnn_build(self._h))
 
+    def gnn_launches(self) -> int:
+        """Kernel launches of one GNN forward: per constant-bank chunk the CTA
+        kernel, one launch per cluster size in use, and for flat-path subdomains
+        a restriction prologue (first chunk) plus two launches per layer."""
+        i = self.info()
+        n, nl_max = 0, i["lmax"]
+        for ch in range(i["n_chunks"]):
+            nl = min(nl_max, i["k_bar"] - ch * nl_max)
+            n += (i["K"] > i["n_big"]) + i["cluster_launches"]
+            if i["n_big"] > i["n_cluster"]:
+                n += 2 * nl + (1 if ch == 0 else 0)
+        return n
+
     def info(self) -> dict:
-        out = np.zeros(12, dtype=np.int64)
-        check(self._lib.ddmgnn_info(self._h, i64ptr(out), 12))
+        out = np.zeros(14, dtype=np.int64)
+        check(self._lib.ddmgnn_info(self._h, i64ptr(out), 14))
         keys = ("n", "K", "V", "E", "E_pad", "k_max", "slices", "k_bar", "d", "lmax",
-                "n_chunks", "n_big")
+                "n_chunks", "n_big", "n_cluster", "cluster_launches")
         return dict(zip(keys, (int(x) for x in out)))
 
     def export_local_graph(self, sub: int):

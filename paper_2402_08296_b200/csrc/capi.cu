@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -107,6 +108,8 @@ struct ddmgnn_ctx {
   float *d_hbuf = nullptr, *d_cbuf = nullptr, *d_qbuf = nullptr;
   int2* d_bslices = nullptr;  // flat path: (subdomain, slice) of the oversized subdomains
   int n_bslices = 0;
+  int* d_csubs = nullptr;     // cluster path: subdomains by cluster size 2, 4, 8
+  int cluster_count[3] = {0, 0, 0};
   int *d_bad = nullptr, *d_outbad = nullptr, *d_status = nullptr;
   double *d_rin = nullptr, *d_zout = nullptr;  // host-pointer apply staging
   // pcg
@@ -184,7 +187,7 @@ static void free_layout(ddmgnn_ctx* c) {
   dfree(L.deg); dfree(L.edges); dfree(L.xy); dfree(L.tptr); dfree(L.tent); dfree(L.pou);
   dfree(c->d_r0r); dfree(c->d_scale); dfree(c->d_zloc); dfree(c->d_y);
   dfree(c->d_bad); dfree(c->d_outbad);
-  dfree(c->d_hbuf); dfree(c->d_cbuf); dfree(c->d_qbuf); dfree(c->d_bslices);
+  dfree(c->d_hbuf); dfree(c->d_cbuf); dfree(c->d_qbuf); dfree(c->d_bslices); dfree(c->d_csubs);
   dfree(c->d_ainv); dfree(c->d_ainv_off);
   c->have_asm = false;
   c->n_bslices = 0;
@@ -368,16 +371,38 @@ static int refresh_classes(ddmgnn_ctx* c) {
   const int d = c->model.d;
   c->gnn_smem = gnn_plan_smem(d, c->lay.k_max, &c->cap0);
   const auto& sp = c->lay.h_sub_ptr;
-  // oversized subdomains (k > cap0) lead the LPT order; they take the flat path
+  // oversized subdomains (k > cap0) lead the LPT order: those an 8-CTA cluster can
+  // hold take the cluster path (smallest cluster size whose per-CTA share fits),
+  // the rest (the largest, hence the leading ones) the flat path
+  const char* env = getenv("DDMGNN_CLUSTER");
+  const bool use_cluster = !(env && env[0] == '0');
   int nb = 0;
   std::vector<int2> bsl;
+  std::vector<int> csub[3];
   for (int t = 0; t < c->K; ++t) {
     const int i = c->lay.h_order[t];
     const int k = sp[i + 1] - sp[i];
     if (k <= c->cap0) break;
     ++nb;
-    for (int q = 0; q * 32 < k; ++q) bsl.push_back(make_int2(i, q));
+    int j = -1;
+    for (int jj = 0; use_cluster && jj < 3 && j < 0; ++jj) {
+      const int cs = 2 << jj, npc = ((k + cs - 1) / cs + 31) / 32 * 32;
+      if (npc <= c->cap0) j = jj;
+    }
+    if (j >= 0) {
+      csub[j].push_back(i);
+    } else {
+      for (int q = 0; q * 32 < k; ++q) bsl.push_back(make_int2(i, q));
+    }
   }
+  std::vector<int> cs_all;
+  for (int j = 0; j < 3; ++j) {
+    c->cluster_count[j] = static_cast<int>(csub[j].size());
+    cs_all.insert(cs_all.end(), csub[j].begin(), csub[j].end());
+  }
+  dfree(c->d_csubs);
+  c->d_csubs = nullptr;
+  if (!cs_all.empty()) CUDA_TRY(upload(&c->d_csubs, cs_all));
   c->n_big = nb;
   const int hs = (d % 2 == 0) ? d : d + 1;
   const int qs = (2 * d + 3) / 4 * 4;
@@ -386,7 +411,7 @@ static int refresh_classes(ddmgnn_ctx* c) {
   // + one dummy row per subdomain (lanes past k / SELL padding targets)
   CUDA_TRY(dalloc(&c->d_hbuf, (multi || nb) ? (V + c->K) * hs : 0));
   CUDA_TRY(dalloc(&c->d_cbuf, (multi || nb) ? V : 0));
-  CUDA_TRY(dalloc(&c->d_qbuf, nb ? (V + c->K) * qs : 0));
+  CUDA_TRY(dalloc(&c->d_qbuf, bsl.empty() ? 0 : (V + c->K) * qs));
   dfree(c->d_bslices);
   c->n_bslices = static_cast<int>(bsl.size());
   while (bsl.size() % kFlatWarps) bsl.push_back(make_int2(-1, 0));  // padding slices
@@ -444,9 +469,11 @@ extern "C" int ddmgnn_build(ddmgnn_ctx* c) {
 
 extern "C" int ddmgnn_info(ddmgnn_ctx* c, int64_t* out, int n_out) {
   if (!c) return fail(kValueError, "null context");
-  int64_t v[12] = {c->n, c->K, c->lay.V, c->lay.E, c->lay.E_pad, c->lay.k_max, c->lay.S,
-                   c->model.k_bar, c->model.d, c->model.lmax, c->model.n_chunks(), c->n_big};
-  for (int i = 0; i < n_out && i < 12; ++i) out[i] = v[i];
+  const int ncl = (c->cluster_count[0] > 0) + (c->cluster_count[1] > 0) + (c->cluster_count[2] > 0);
+  int64_t v[14] = {c->n, c->K, c->lay.V, c->lay.E, c->lay.E_pad, c->lay.k_max, c->lay.S,
+                   c->model.k_bar, c->model.d, c->model.lmax, c->model.n_chunks(), c->n_big,
+                   c->cluster_count[0] + c->cluster_count[1] + c->cluster_count[2], ncl};
+  for (int i = 0; i < n_out && i < 14; ++i) out[i] = v[i];
   return kOk;
 }
 
@@ -523,6 +550,8 @@ static cudaError_t enqueue_gnn(ddmgnn_ctx* c, const double* r, int* status, cons
   a.r = r; a.r0r = c->d_r0r; a.scale = c->d_scale; a.zloc = c->d_zloc;
   a.hbuf = c->d_hbuf; a.cbuf = c->d_cbuf; a.qbuf = c->d_qbuf;
   a.bslices = c->d_bslices; a.n_bslices = c->n_bslices;
+  a.csubs = c->d_csubs;
+  for (int j = 0; j < 3; ++j) a.cluster_count[j] = c->cluster_count[j];
   a.bad_layer = c->d_bad; a.out_bad = c->d_outbad; a.status = status; a.skip = skip;
   a.alpha = M.alpha;
   const int nch = M.n_chunks();

@@ -142,6 +142,8 @@ struct GnnArgs {
   int cap0;          // largest subdomain of the shared-memory CTA path (gnn_plan_smem)
   const int2* bslices;  // flat path: (subdomain, slice) of every slice of a big subdomain
   int n_bslices;
+  const int* csubs;     // cluster path: subdomains of one cluster-size class
+  int cluster_count[3];  // subdomains per cluster size 2, 4, 8 (csubs laid out in that order)
 };
 int gnn_smem_max_nodes(int d);
 // WQ WP B1 WL WU BP1 WP2 BP2 STRIDE D2P DP DEC_W1 DEC_B1 DEC_W2 DEC_B2 LMAX (gnn_cfg.h)

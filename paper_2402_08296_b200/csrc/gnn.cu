@@ -117,7 +117,7 @@ cudaError_t launch_gnn(int d, int n_ctas, int n_big, int k_max_small, size_t sme
     if ((e = cudaEventRecord(fork, s)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(side, fork, 0)) != cudaSuccess) return e;
     switch (d) {
-#define X(DD) case DD: e = gnn_launch_big_d##DD(n_big, 0, 0, a, side); break;
+#define X(DD) case DD: e = gnn_launch_big_d##DD(n_big, 0, smem, a, side); break;
       DDM_GNN_DIMS(X)
 #undef X
       default: return cudaErrorInvalidValue;

@@ -50,7 +50,10 @@ cudaError_t DDM_NAME(gnn_launch)(int n_ctas, int k_max, size_t smem, const GnnAr
 
 #else
 
-cudaError_t DDM_NAME(gnn_configure)() { return cudaSuccess; }
+cudaError_t DDM_NAME(gnn_configure)() {
+  return cudaFuncSetAttribute(gnn_cluster_kernel<GNN_D>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, kGnnSmemMax);
+}
 
 namespace {
 using QFn = void (*)(GnnArgs);
@@ -67,21 +70,49 @@ constexpr UFn ufn() {
 }
 }  // namespace
 
-// Flat path over the n_subs oversized subdomains order[a.order_begin ...]:
-// restriction (first chunk), then per layer of the chunk one launch per phase over
-// all a.n_bslices slices.
-cudaError_t DDM_NAME(gnn_launch)(int n_subs, int /*k_max*/, size_t /*smem*/, const GnnArgs& a,
+// Oversized subdomains order[a.order_begin ...]: the first n_flat = n_subs -
+// sum(a.cluster_count) (too large for an 8-CTA cluster) through the flat path —
+// restriction (first chunk), then per layer one launch per phase over all
+// a.n_bslices slices — then one cluster launch per cluster size 2, 4, 8 over
+// a.csubs (smem = dynamic shared memory per CTA).
+cudaError_t DDM_NAME(gnn_launch)(int n_subs, int /*k_max*/, size_t smem, const GnnArgs& a,
                                  cudaStream_t s) {
   static const QFn qk[10] = {qfn<0>(), qfn<1>(), qfn<2>(), qfn<3>(), qfn<4>(),
                              qfn<5>(), qfn<6>(), qfn<7>(), qfn<8>(), qfn<9>()};
   static const UFn uk[10] = {ufn<0>(), ufn<1>(), ufn<2>(), ufn<3>(), ufn<4>(),
                              ufn<5>(), ufn<6>(), ufn<7>(), ufn<8>(), ufn<9>()};
-  if (n_subs <= 0 || a.n_bslices <= 0) return cudaSuccess;
-  if (a.first) gnn_flat_prologue<GNN_D><<<n_subs, kGnnThreads, 0, s>>>(a);
-  for (int l = 0; l < a.nl; ++l) {
-    const int blocks = (a.n_bslices + kFlatWarps - 1) / kFlatWarps;  // table padded
-    qk[l]<<<blocks, 32 * kFlatWarps, 0, s>>>(a);
-    uk[l]<<<blocks, 32 * kFlatWarps, 0, s>>>(a, a.layer0 + l, a.last && l == a.nl - 1);
+  const int n_cl = a.cluster_count[0] + a.cluster_count[1] + a.cluster_count[2];
+  const int n_flat = n_subs - n_cl;
+  if (n_flat > 0 && a.n_bslices > 0) {
+    if (a.first) gnn_flat_prologue<GNN_D><<<n_flat, kGnnThreads, 0, s>>>(a);
+    for (int l = 0; l < a.nl; ++l) {
+      const int blocks = (a.n_bslices + kFlatWarps - 1) / kFlatWarps;  // table padded
+      qk[l]<<<blocks, 32 * kFlatWarps, 0, s>>>(a);
+      uk[l]<<<blocks, 32 * kFlatWarps, 0, s>>>(a, a.layer0 + l, a.last && l == a.nl - 1);
+    }
+  }
+  int off = 0;
+  for (int j = 0; j < 3; ++j) {
+    const int cnt = a.cluster_count[j];
+    if (cnt <= 0) continue;
+    const unsigned cs = 2u << j;
+    GnnArgs m = a;
+    m.csubs = a.csubs + off;
+    off += cnt;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cnt * cs);
+    cfg.blockDim = dim3(kGnnThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, gnn_cluster_kernel<GNN_D>, m);
+    if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
 }

@@ -29,6 +29,8 @@
 // slot), with the weight pair as a uniform-register operand loaded by LDCU.128
 // from a 64 KB __constant__ bank (layer slot = uniform base register + immediate).
 #pragma once
+#include <cooperative_groups.h>
+
 #include <climits>
 
 #include "ddmgnn_internal.h"
@@ -198,14 +200,21 @@ __device__ __forceinline__ void slice_q2(int n0a, int n0b, int k, const float* h
   store_vec<C::QS>(q + nb * C::QS, qsb);
 }
 
+// Q-row addressing of phase B: rows of the CTA's own shared memory ...
+struct LocalRows {
+  const float* q;
+  template <int QS>
+  __device__ __forceinline__ void load(int t, float (&v)[QS]) const { load_vec<QS>(q + t * QS, v); }
+};
+
 // phase B: edge aggregation + node update; returns whether the lane's node became
 // non-finite and leaves the updated latent in hn (for a fused decoder)
-template <int D, int W>
-__device__ __forceinline__ bool slice_u(int n0, int k, float* h, const float* q,
+template <int D, int W, class Rows = LocalRows>
+__device__ __forceinline__ bool slice_u(int n0, int k, float* h, Rows q,
                                         const float* c, const float2* __restrict__ xy,
                                         const float2* __restrict__ edges, int so, int width,
                                         const uint16_t* __restrict__ deg, float alpha,
-                                        float (&hn)[Cfg<D>::DH]) {
+                                        float (&hn)[Cfg<D>::DH], int kdummy = -1) {
   using C = Cfg<D>;
   constexpr int NP2 = C::NP2, NPH = C::NPH;
   const int lane = threadIdx.x & 31;
@@ -222,14 +231,14 @@ __device__ __forceinline__ bool slice_u(int n0, int k, float* h, const float* q,
     }
     mv2<D + 2, NP2, W + C::OFF_WP, C::D2P>(0, hin, p);
   }
-  const float2 dummy = make_float2(0.f, __int_as_float(k));
+  const float2 dummy = make_float2(0.f, __int_as_float(kdummy < 0 ? k : kdummy));
   const float2* ep = edges + so + lane;
   float2 rec = width > 0 ? __ldg(ep) : dummy;
   for (int e = 0; e < width; ++e) {
     const float2 cur = rec;
     rec = e + 1 < width ? __ldg(ep + 32 * (e + 1)) : dummy;
     float qt[C::QS];
-    load_vec<C::QS>(q + __float_as_int(cur.y) * C::QS, qt);
+    q.template load<C::QS>(__float_as_int(cur.y), qt);
     const float2 len = bcast(cur.x);
 #pragma unroll
     for (int j = 0; j < NP2; ++j) {
@@ -766,7 +775,8 @@ __device__ __forceinline__ void cta_layer(const SmemState<D>& ns, int k, int war
     const int so = uni(slice_off[n0 >> 5]);
     const int width = (uni(slice_off[(n0 >> 5) + 1]) - so) >> 5;
     float hn[Cfg<D>::DH];
-    const bool b = slice_u<D, W>(n0, k, ns.h, ns.q, ns.c, xy, edges, so, width, deg, alpha, hn);
+    const bool b = slice_u<D, W>(n0, k, ns.h, LocalRows{ns.q}, ns.c, xy, edges, so, width, deg,
+                                 alpha, hn);
     if (b && first_bad == 0) first_bad = layer_no;
   }
   if (first_bad != 0 && *bad == 0) *bad = first_bad;
@@ -1007,7 +1017,7 @@ __global__ void __launch_bounds__(32 * kFlatWarps) gnn_flat_u(GnnArgs a, int lay
   const int width = (uni(so_p[1]) - so) >> 5;
   float hn[C::DH];
   const bool bad = slice_u<D, W>(f.n0, f.k, a.hbuf + static_cast<size_t>(f.pos0 + f.sub) * C::HS,
-                                 a.qbuf + static_cast<size_t>(f.pos0 + f.sub) * C::QS,
+                                 LocalRows{a.qbuf + static_cast<size_t>(f.pos0 + f.sub) * C::QS},
                                  a.cbuf + f.pos0, a.xy + f.pos0, a.edges, so, width,
                                  a.deg + f.pos0, a.alpha, hn);
   // layers run in order (one launch each), so the first non-zero wins
@@ -1024,6 +1034,195 @@ __global__ void __launch_bounds__(32 * kFlatWarps) gnn_flat_u(GnnArgs a, int lay
         atomicMax(a.status, static_cast<int>(kPrecondError));
       }
       a.zloc[f.pos0 + n] = f.s * static_cast<double>(o);
+    }
+  }
+}
+
+
+// ---------------------------------------------------------------------------- cluster path
+// Subdomains up to 8x the shared-memory capacity of one CTA: a thread-block cluster
+// of CS CTAs per subdomain, CTA r holding the node state of local nodes
+// [r npc, (r+1) npc) in its shared memory; phase B reads neighbours' Q rows through
+// distributed shared memory (cluster.map_shared_rank), phases are separated by
+// cluster barriers, and the restriction sums meet in CTA 0.  Same per-node
+// arithmetic as the CTA path.
+struct ClusterRows {
+  uint32_t q;  // shared-window address of this CTA's Q rows (same offset in every CTA)
+  int npc, last;
+  float inv_npc;
+  template <int QS>
+  __device__ __forceinline__ void load(int t, float (&v)[QS]) const {
+    static_assert(QS % 4 == 0, "Q rows are float4-aligned");
+    int r = __float2int_rz(__int2float_rn(t) * inv_npc);
+    r -= (r * npc > t);
+    r += ((r + 1) * npc <= t);
+    r = min(r, last);
+    uint32_t a;
+    asm("mapa.shared::cluster.u32 %0, %1, %2;"
+        : "=r"(a) : "r"(q + static_cast<uint32_t>((t - r * npc) * QS * 4)), "r"(r));
+#pragma unroll
+    for (int i = 0; i < QS; i += 4)
+      asm("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=f"(v[i]), "=f"(v[i + 1]), "=f"(v[i + 2]), "=f"(v[i + 3])
+                   : "r"(a + 4 * i));
+  }
+};
+
+template <int D>
+__global__ void __launch_bounds__(kGnnThreads, 1) gnn_cluster_kernel(GnnArgs a) {
+  using C = Cfg<D>;
+  namespace cg = cooperative_groups;
+  if (a.skip != nullptr && uni(*a.skip) != 0) return;  // same flag for the whole cluster
+  __shared__ GnnShared sh;
+  __shared__ double cpart[2][8];
+  __shared__ int cbad;
+  cg::cluster_group cl = cg::this_cluster();
+  const int CS = static_cast<int>(cl.num_blocks()), rank = static_cast<int>(cl.block_rank());
+  const int sub = uni(a.csubs[blockIdx.x / CS]);
+  const int pos0 = uni(a.sub_ptr[sub]);
+  const int k = uni(a.sub_ptr[sub + 1] - pos0);
+  const int npc = ((k + CS - 1) / CS + 31) / 32 * 32;
+  const int lo = rank * npc;
+  const int cnt = max(0, min(k - lo, npc));
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  SmemState<D> ns(npc);
+  if (tid == 0) {
+    sh.bad = 0;
+    cbad = INT_MAX;
+  }
+  double s;
+  if (a.first) {
+    double* scratch = reinterpret_cast<double*>(ns.q);
+    double ss = 0.0, rr0 = 0.0;
+    for (int n = tid; n < cnt; n += nthr) {
+      const int g = a.idx[pos0 + lo + n];
+      const double v = a.r[g];
+      ss = fma(v, v, ss);
+      rr0 = fma(a.pou[g], v, rr0);
+      scratch[n] = v;
+    }
+    ss = warp_sum(ss);
+    rr0 = warp_sum(rr0);
+    if ((tid & 31) == 0) {
+      sh.red[0][tid >> 5] = ss;
+      sh.red[1][tid >> 5] = rr0;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double t0 = 0.0, t1 = 0.0;
+      for (int w = 0; w < (nthr >> 5); ++w) {
+        t0 += sh.red[0][w];
+        t1 += sh.red[1][w];
+      }
+      double* dst = cl.map_shared_rank(&cpart[0][0], 0);
+      dst[rank] = t0;
+      dst[8 + rank] = t1;
+    }
+    cl.sync();
+    if (tid == 0) {
+      const double* src = cl.map_shared_rank(&cpart[0][0], 0);
+      double t0 = 0.0, t1 = 0.0;
+      for (int j = 0; j < CS; ++j) {
+        t0 += src[j];
+        t1 += src[8 + j];
+      }
+      sh.scale = sqrt(t0);
+      if (rank == 0) {
+        a.scale[sub] = sh.scale;
+        a.r0r[sub] = t1;
+        a.bad_layer[sub] = 0;
+        a.out_bad[sub] = 0;
+      }
+    }
+    cl.sync();  // CTA 0's partials read by everyone before anyone may leave
+    s = __shfl_sync(0xffffffffu, sh.scale, 0);
+    if (s == 0.0) return;
+    for (int n = tid; n < cnt; n += nthr) {
+      const float c = static_cast<float>(scratch[n] / s);
+      ns.c[n] = c;
+      if (!a.last) a.cbuf[pos0 + lo + n] = c;
+    }
+    __syncthreads();
+    for (int n = tid; n < cnt; n += nthr) {
+      float z[C::DH];
+#pragma unroll
+      for (int i = 0; i < C::DH; ++i) z[i] = 0.f;
+      store_vec<C::DH>(ns.h + n * C::HS, z);
+    }
+  } else {
+    s = __shfl_sync(0xffffffffu, a.scale[sub], 0);
+    if (s == 0.0) return;
+    for (int n = tid; n < cnt; n += nthr) {
+      ns.c[n] = a.cbuf[pos0 + lo + n];
+      float hv[C::DH];
+      load_vec<C::DH>(a.hbuf + static_cast<size_t>(pos0 + sub + lo + n) * C::HS, hv);
+      store_vec<C::DH>(ns.h + n * C::HS, hv);
+    }
+  }
+  // dummy Q row: the SELL padding target t = k lands in the last CTA at row cnt
+  for (int j = tid; j < C::QS; j += nthr) ns.q[static_cast<size_t>(cnt) * C::QS + j] = -1e30f;
+  cl.sync();
+  {
+    const int warp = uni(tid >> 5);
+    const float2* xy = a.xy + pos0 + lo;
+    const int* so_p = a.slice_off + a.slice_base[sub] + (lo >> 5);
+    const uint16_t* dg = a.deg + pos0 + lo;
+    const ClusterRows rows{static_cast<uint32_t>(__cvta_generic_to_shared(ns.q)), npc, CS - 1,
+                           1.0f / static_cast<float>(npc)};
+    const int nsl = (cnt + 31) >> 5, half = (nsl + 1) >> 1;
+#define DDM_CLAYER(LL)                                                                        \
+  if constexpr (LL < C::LMAX) {                                                               \
+    if (LL < a.nl) {                                                                          \
+      for (int sa = warp; sa < half; sa += nthr >> 5) {                                       \
+        const int sb = sa + half < nsl ? sa + half : sa;                                      \
+        slice_q2<D, LL * C::STRIDE>(sa * 32, sb * 32, cnt, ns.h, ns.q, xy);                   \
+      }                                                                                       \
+      cl.sync();                                                                              \
+      int fb = 0;                                                                             \
+      for (int n0 = 32 * warp; n0 < cnt; n0 += nthr) {                                        \
+        const int so = uni(so_p[n0 >> 5]);                                                    \
+        const int width = (uni(so_p[(n0 >> 5) + 1]) - so) >> 5;                               \
+        float hn[C::DH];                                                                      \
+        const bool b = slice_u<D, LL * C::STRIDE, ClusterRows>(                               \
+            n0, cnt, ns.h, rows, ns.c, xy, a.edges, so, width, dg, a.alpha, hn, k);           \
+        if (b && fb == 0) fb = a.layer0 + LL;                                                 \
+      }                                                                                       \
+      if (fb != 0 && sh.bad == 0) sh.bad = fb;                                                \
+      cl.sync();                                                                              \
+    }                                                                                         \
+  }
+    DDM_CLAYER(0) DDM_CLAYER(1) DDM_CLAYER(2) DDM_CLAYER(3) DDM_CLAYER(4)
+    DDM_CLAYER(5) DDM_CLAYER(6) DDM_CLAYER(7) DDM_CLAYER(8) DDM_CLAYER(9)
+#undef DDM_CLAYER
+  }
+  int outbad = 0;
+  if (a.last) {
+    for (int n = tid; n < cnt; n += nthr) {
+      float hv[C::DH];
+      load_vec<C::DH>(ns.h + n * C::HS, hv);
+      const float o = decode<D>(hv);
+      if (!isfinite(o)) outbad = 1;
+      a.zloc[pos0 + lo + n] = s * static_cast<double>(o);
+    }
+  } else {
+    for (int n = tid; n < cnt; n += nthr) {
+      float hv[C::DH];
+      load_vec<C::DH>(ns.h + n * C::HS, hv);
+      store_vec<C::DH>(a.hbuf + static_cast<size_t>(pos0 + sub + lo + n) * C::HS, hv);
+    }
+  }
+  outbad = __syncthreads_or(outbad);
+  // combine the CTAs' flags in CTA 0: first (smallest) bad layer, any bad output
+  if (tid == 0 && sh.bad != 0) atomicMin(cl.map_shared_rank(&cbad, 0), sh.bad);
+  cl.sync();
+  if (tid == 0) {
+    if (outbad) {
+      a.out_bad[sub] = 1;
+      atomicMax(a.status, static_cast<int>(kPrecondError));
+    }
+    if (rank == 0 && cbad != INT_MAX) {
+      if (a.first || a.bad_layer[sub] == 0) a.bad_layer[sub] = cbad;
+      atomicMax(a.status, static_cast<int>(kPrecondError));
     }
   }
 }

@@ -418,12 +418,8 @@ class ShardedDdmGnn:
 
     def launches_per_apply(self) -> int:
         """Kernels of libddmgnn_b200 launched by one apply_owned."""
-        info = self.ctx.info()
         multi = self.comm.size > 1
-        gnn = 0
-        for ch in range(info["n_chunks"]):
-            nl = min(info["lmax"], info["k_bar"] - ch * info["lmax"])
-            gnn += 1 + ((2 * nl + (1 if ch == 0 else 0)) if info["n_big"] else 0)
+        gnn = self.ctx.gnn_launches()
         return (1 + 2 * multi) + gnn + 4 + (self.kinv is not None) + multi + 1
 
     # -- helpers --------------------------------------------------------------------------

@@ -132,8 +132,21 @@ def test_multi_chunk_model_matches_oracle(ddm):
         assert rel_l2(p(r), orc.OraclePreconditioner(a, coords, dec.subdomains, om, "two")(r)) < TOL
 
 
-def test_large_subdomains_use_global_variant(ddm):
-    """Subdomains too large for shared memory run the global-scratch kernel."""
+@pytest.fixture(params=["cluster", "flat"])
+def big_path(request, monkeypatch):
+    """Oversized subdomains: thread-block-cluster path (default) or, with
+    DDMGNN_CLUSTER=0, the flat node-parallel path."""
+    monkeypatch.setenv("DDMGNN_CLUSTER", "1" if request.param == "cluster" else "0")
+    return request.param
+
+
+def _check_path(info, path):
+    assert info["n_big"] >= 1
+    assert (info["n_cluster"] == info["n_big"]) if path == "cluster" else info["n_cluster"] == 0
+
+
+def test_large_subdomains_use_global_variant(ddm, big_path):
+    """Subdomains too large for one CTA's shared memory (cluster or flat path)."""
     from oracle import ddm_oracle as orc
 
     g = load_golden("A.npz")
@@ -143,7 +156,7 @@ def test_large_subdomains_use_global_variant(ddm):
     dec2 = ddm.finish_decomposition(merged, dec.base_owner, dec.overlap)
     model = ddm.init_model(10, 10, seed=1)
     p = ddm.build_ddm_gnn(a, coords, dec2, model, level="one")
-    assert p.info()["n_big"] >= 1
+    _check_path(p.info(), big_path)
     om = orc.model_from_flat(10, 10, model.alpha, 1, ddm.flat_params(model))
     ref = orc.OraclePreconditioner(a, coords, merged, om, "one")
     assert rel_l2(p(g["r"]), ref(g["r"])) < TOL
@@ -158,7 +171,7 @@ def _merged_config_a(ddm):
 
 
 @pytest.mark.parametrize("k_bar", [10, 30])
-def test_flat_path_two_level_deep_model(ddm, k_bar):
+def test_flat_path_two_level_deep_model(ddm, k_bar, big_path):
     """Oversized subdomains (flat node-parallel path), two-level, and a model deep
     enough for several constant-bank chunks, against the oracle."""
     from oracle import ddm_oracle as orc
@@ -167,19 +180,20 @@ def test_flat_path_two_level_deep_model(ddm, k_bar):
     model = ddm.init_model(k_bar, 10, seed=2)
     p = ddm.build_ddm_gnn(a, coords, dec2, model, level="two")
     info = p.info()
-    assert info["n_big"] >= 1 and (k_bar < 11 or info["n_chunks"] > 1)
+    _check_path(info, big_path)
+    assert k_bar < 11 or info["n_chunks"] > 1
     om = orc.model_from_flat(k_bar, 10, model.alpha, 2, ddm.flat_params(model))
     ref = orc.OraclePreconditioner(a, coords, merged, om, "two")
     assert rel_l2(p(g["r"]), ref(g["r"])) < TOL
     assert np.array_equal(p(g["r"]), p(g["r"]))
 
 
-def test_flat_path_reports_non_finite_states(ddm):
+def test_flat_path_reports_non_finite_states(ddm, big_path):
     g, a, coords, dec2, _merged = _merged_config_a(ddm)
     model = ddm.init_model(3, 10, seed=1)
     model.layers[1].psi.b2[...] = np.inf
     p = ddm.build_ddm_gnn(a, coords, dec2, model)
-    assert p.info()["n_big"] >= 1
+    _check_path(p.info(), big_path)
     with pytest.raises(RuntimeError, match="non-finite latent state at message-passing iteration 2"):
         p(g["r"])
     model = ddm.init_model(2, 10, seed=4)
