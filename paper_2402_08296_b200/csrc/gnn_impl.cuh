@@ -735,7 +735,7 @@ __device__ __forceinline__ void tc_layer(const SmemState<D>& ns, int k, int warp
     store_vec<C::DH>(ns.h + min(n, k) * C::HS, hn);
     asm volatile("tcgen05.fence::before_thread_sync;");
   }
-  if (first_bad != 0 && *bad == 0) *bad = first_bad;
+  if (first_bad != 0) atomicCAS(bad, 0, first_bad);  // first bad layer wins
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
 }
@@ -779,7 +779,7 @@ __device__ __forceinline__ void cta_layer(const SmemState<D>& ns, int k, int war
                                  alpha, hn);
     if (b && first_bad == 0) first_bad = layer_no;
   }
-  if (first_bad != 0 && *bad == 0) *bad = first_bad;
+  if (first_bad != 0) atomicCAS(bad, 0, first_bad);  // first bad layer wins
   __syncthreads();
 }
 
@@ -1107,7 +1107,7 @@ __global__ void __launch_bounds__(kGnnThreads, 1) gnn_cluster_kernel(GnnArgs a) 
       sh.red[0][tid >> 5] = ss;
       sh.red[1][tid >> 5] = rr0;
     }
-    __syncthreads();
+    cl.sync();  // also: every CTA of the cluster has started before DSMEM is written
     if (tid == 0) {
       double t0 = 0.0, t1 = 0.0;
       for (int w = 0; w < (nthr >> 5); ++w) {
@@ -1187,7 +1187,7 @@ __global__ void __launch_bounds__(kGnnThreads, 1) gnn_cluster_kernel(GnnArgs a) 
             n0, cnt, ns.h, rows, ns.c, xy, a.edges, so, width, dg, a.alpha, hn, k);           \
         if (b && fb == 0) fb = a.layer0 + LL;                                                 \
       }                                                                                       \
-      if (fb != 0 && sh.bad == 0) sh.bad = fb;                                                \
+      if (fb != 0) atomicCAS(&sh.bad, 0, fb); /* first bad layer wins */                    \
       cl.sync();                                                                              \
     }                                                                                         \
   }

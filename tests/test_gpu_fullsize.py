@@ -78,3 +78,31 @@ def test_config_c_spmv_bitwise(ddm, config_c):
     p.context.spmv_device(xd.data_ptr(), yd.data_ptr(), st)
     torch.cuda.synchronize()
     assert np.array_equal(yd.cpu().numpy(), a @ x)
+
+
+@pytest.mark.parametrize("ns,cs", [(2000, 2), (5000, 4), (10000, 8)])
+def test_config_e_cluster_matches_flat(ddm, monkeypatch, ns, cs):
+    """Config E subdomain sizes beyond one CTA's shared memory: the 2/4/8-CTA
+    cluster path against the flat path (same per-node arithmetic; only the
+    restriction norm's summation order differs) and its own repeatability."""
+    import torch
+
+    prob = _build(50 * ns, ns=ns, overlap=2)
+    model = ddm.init_model(10, 10, seed=1)
+    r = torch.tensor(np.random.default_rng(0).standard_normal(prob.system.n), device="cuda")
+    out = {}
+    for path in ("1", "0"):
+        monkeypatch.setenv("DDMGNN_CLUSTER", path)
+        p = ddm.build_ddm_gnn(prob.system.a, prob.coords, prob.dec, model)
+        info = p.info()
+        assert info["n_big"] == info["K"]
+        if path == "1":
+            assert info["n_cluster"] == info["K"] and info["cluster_launches"] >= 1
+            assert info["k_max"] > (cs // 2) * 1400  # sized to need a cluster of cs CTAs
+        else:
+            assert info["n_cluster"] == 0
+        out[path] = p(r)
+        if path == "1":
+            assert torch.equal(out[path], p(r))
+    z1, z0 = out["1"].cpu().numpy(), out["0"].cpu().numpy()
+    assert rel_l2(z1, z0) < 1e-6

@@ -39,7 +39,7 @@ def raw(rep):
 def main():
     traffic = {}
     summary_rows = []
-    for k in ("gnn_kernel", "gnn_flat_u", "spmv_kernel"):
+    for k in ("gnn_kernel", "gnn_cluster_kernel", "gnn_flat_u", "spmv_kernel"):
         rep = os.path.join(OUT, f"{R}_{k}.ncu-rep")
         if not os.path.exists(rep):
             continue
