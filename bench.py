@@ -432,7 +432,7 @@ def run_ours(args):
                 "parallelism": f"{world} rank(s); each rank owns a full config-C instance",
             },
             "roofline": {
-                "kernel": "gnn_kernel + concurrent gnn_big_kernel (fused restriction + "
+                "kernel": "gnn_kernel + concurrent gnn_cluster_kernel (fused restriction + "
                           f"{info['k_bar']} message-passing layers + decoder)",
                 "bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
                 "frac": achieved / fp32_peak, "traffic": gnn_traffic,
