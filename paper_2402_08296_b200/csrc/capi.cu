@@ -110,6 +110,7 @@ struct ddmgnn_ctx {
   int n_bslices = 0;
   int* d_csubs = nullptr;     // cluster path: subdomains by cluster size 2, 4, 8
   int cluster_count[3] = {0, 0, 0};
+  int cluster_smem[3] = {0, 0, 0}, cluster_threads[3] = {0, 0, 0};
   int *d_bad = nullptr, *d_outbad = nullptr, *d_status = nullptr;
   double *d_rin = nullptr, *d_zout = nullptr;  // host-pointer apply staging
   // pcg
@@ -374,8 +375,20 @@ static int refresh_classes(ddmgnn_ctx* c) {
   // oversized subdomains (k > cap0) lead the LPT order: those an 8-CTA cluster can
   // hold take the cluster path (smallest cluster size whose per-CTA share fits),
   // the rest (the largest, hence the leading ones) the flat path
+  // With DDMGNN_CLUSTER_2CTA=1 the cluster size is the smallest whose per-CTA
+  // share fits half an SM's shared memory, so two cluster CTAs (448 threads each)
+  // share each SM — measured slower than the smallest fitting cluster (twice the
+  // DSMEM traffic; profiles/r01_cluster_2cta_configE.jsonl), hence opt-in.
   const char* env = getenv("DDMGNN_CLUSTER");
   const bool use_cluster = !(env && env[0] == '0');
+  const char* env2 = getenv("DDMGNN_CLUSTER_2CTA");
+  const bool two_cta = env2 && env2[0] == '1';
+  const int node0 = gnn_smem_node_bytes(d);
+  constexpr int kClusterStatic = 1024;  // GnnShared + partial sums, rounded up
+  constexpr int kSmPerCtaReserve = 1024;
+  const int cap2 = node0 ? (228 * 1024 / 2 - kClusterStatic - kSmPerCtaReserve -
+                            static_cast<int>(kTcSmemBytes)) / node0 - 1
+                         : 0;
   int nb = 0;
   std::vector<int2> bsl;
   std::vector<int> csub[3];
@@ -385,10 +398,11 @@ static int refresh_classes(ddmgnn_ctx* c) {
     if (k <= c->cap0) break;
     ++nb;
     int j = -1;
-    for (int jj = 0; use_cluster && jj < 3 && j < 0; ++jj) {
-      const int cs = 2 << jj, npc = ((k + cs - 1) / cs + 31) / 32 * 32;
-      if (npc <= c->cap0) j = jj;
-    }
+    for (int pass = two_cta ? 0 : 1; use_cluster && pass < 2 && j < 0; ++pass)
+      for (int jj = 0; jj < 3 && j < 0; ++jj) {
+        const int cs = 2 << jj, npc = ((k + cs - 1) / cs + 31) / 32 * 32;
+        if (npc <= (pass == 0 ? cap2 : c->cap0)) j = jj;
+      }
     if (j >= 0) {
       csub[j].push_back(i);
     } else {
@@ -398,6 +412,15 @@ static int refresh_classes(ddmgnn_ctx* c) {
   std::vector<int> cs_all;
   for (int j = 0; j < 3; ++j) {
     c->cluster_count[j] = static_cast<int>(csub[j].size());
+    int npc_max = 0;
+    for (int i : csub[j]) {
+      const int k = sp[i + 1] - sp[i], cs = 2 << j;
+      npc_max = std::max(npc_max, ((k + cs - 1) / cs + 31) / 32 * 32);
+    }
+    const size_t sm = static_cast<size_t>(npc_max + 1) * node0 + kTcSmemBytes;
+    c->cluster_smem[j] = static_cast<int>(std::min<size_t>(sm, kGnnSmemMax));
+    const bool pair = 2 * (sm + kClusterStatic + kSmPerCtaReserve) <= 228u * 1024u;
+    c->cluster_threads[j] = (two_cta && pair) ? kGnnThreads / 2 / 32 * 32 : kGnnThreads;
     cs_all.insert(cs_all.end(), csub[j].begin(), csub[j].end());
   }
   dfree(c->d_csubs);
@@ -551,7 +574,11 @@ static cudaError_t enqueue_gnn(ddmgnn_ctx* c, const double* r, int* status, cons
   a.hbuf = c->d_hbuf; a.cbuf = c->d_cbuf; a.qbuf = c->d_qbuf;
   a.bslices = c->d_bslices; a.n_bslices = c->n_bslices;
   a.csubs = c->d_csubs;
-  for (int j = 0; j < 3; ++j) a.cluster_count[j] = c->cluster_count[j];
+  for (int j = 0; j < 3; ++j) {
+    a.cluster_count[j] = c->cluster_count[j];
+    a.cluster_smem[j] = c->cluster_smem[j];
+    a.cluster_threads[j] = c->cluster_threads[j];
+  }
   a.bad_layer = c->d_bad; a.out_bad = c->d_outbad; a.status = status; a.skip = skip;
   a.alpha = M.alpha;
   const int nch = M.n_chunks();

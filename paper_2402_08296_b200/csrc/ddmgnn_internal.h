@@ -144,6 +144,8 @@ struct GnnArgs {
   int n_bslices;
   const int* csubs;     // cluster path: subdomains of one cluster-size class
   int cluster_count[3];  // subdomains per cluster size 2, 4, 8 (csubs laid out in that order)
+  int cluster_smem[3];   // dynamic shared memory per CTA of each cluster-size class
+  int cluster_threads[3];  // threads per CTA (448 when two CTAs fit an SM, else kGnnThreads)
 };
 int gnn_smem_max_nodes(int d);
 // WQ WP B1 WL WU BP1 WP2 BP2 STRIDE D2P DP DEC_W1 DEC_B1 DEC_W2 DEC_B2 LMAX (gnn_cfg.h)

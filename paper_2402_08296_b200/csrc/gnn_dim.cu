@@ -87,8 +87,8 @@ constexpr UFn ufn() {
 // sum(a.cluster_count) (too large for an 8-CTA cluster) through the flat path —
 // restriction (first chunk), then per layer one launch per phase over all
 // a.n_bslices slices — then one cluster launch per cluster size 2, 4, 8 over
-// a.csubs (smem = dynamic shared memory per CTA).
-cudaError_t DDM_NAME(gnn_launch)(int n_subs, int /*k_max*/, size_t smem, const GnnArgs& a,
+// a.csubs (shared memory and threads per CTA planned per class by the host).
+cudaError_t DDM_NAME(gnn_launch)(int n_subs, int /*k_max*/, size_t /*smem*/, const GnnArgs& a,
                                  cudaStream_t s) {
   static const QFn qk[10] = {qfn<0>(), qfn<1>(), qfn<2>(), qfn<3>(), qfn<4>(),
                              qfn<5>(), qfn<6>(), qfn<7>(), qfn<8>(), qfn<9>()};
@@ -114,8 +114,8 @@ cudaError_t DDM_NAME(gnn_launch)(int n_subs, int /*k_max*/, size_t smem, const G
     off += cnt;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cnt * cs);
-    cfg.blockDim = dim3(kGnnThreads);
-    cfg.dynamicSmemBytes = smem;
+    cfg.blockDim = dim3(a.cluster_threads[j]);
+    cfg.dynamicSmemBytes = a.cluster_smem[j];
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
