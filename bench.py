@@ -25,6 +25,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import signal
 import statistics
 import subprocess
 import sys
@@ -115,6 +116,16 @@ class ClockSampler:
         except FileNotFoundError:
             self._proc = None
         return self
+
+    def pause(self):
+        """Stop polling (SIGSTOP) while host-timed work runs: an nvidia-smi query
+        holds the driver for milliseconds and would land inside host-clocked steps."""
+        if self._proc:
+            self._proc.send_signal(signal.SIGSTOP)
+
+    def resume(self):
+        if self._proc:
+            self._proc.send_signal(signal.SIGCONT)
 
     def _read(self):
         for line in self._proc.stdout:
@@ -367,13 +378,18 @@ def run_ours(args):
     r_pin = torch.from_numpy(np.random.default_rng(rank).standard_normal(n)).pin_memory()
     z_pin = torch.empty(n, dtype=torch.float64).pin_memory()
     r_host, z_host = r_pin.numpy(), z_pin.numpy()
-    for _ in range(2):
+    # host-clocked, so more steps than the device-timed loop (short host-timed
+    # loops are noisy: CPU clock ramp, scheduler)
+    e2e_steps = max(args.steps, 100)
+    for _ in range(max(args.warmup, 10)):
         ctx.apply_host(r_host, lvl, out=z_host)
+    clk.pause()
     barrier()
     t0 = time.perf_counter()
-    for _ in range(args.steps):
+    for _ in range(e2e_steps):
         ctx.apply_host(r_host, lvl, out=z_host)
-    t_e2e = (time.perf_counter() - t0) / args.steps
+    t_e2e = (time.perf_counter() - t0) / e2e_steps
+    clk.resume()
     e2e_t = torch.tensor([t_e2e], device=dev)
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
@@ -452,7 +468,7 @@ def run_ours(args):
                 "peak_source": hbm_src,
             },
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
+            "e2e": {"value": e2e_value, "unit": UNIT, "steps": e2e_steps, "h2d_bytes_per_step": 8 * n,
                     "d2h_bytes_per_step": 8 * n},
             "gpu_launches": per_step_launches * args.steps,
             "clocks": clocks,
