@@ -111,6 +111,7 @@ struct ddmgnn_ctx {
   int* d_csubs = nullptr;     // cluster path: subdomains by cluster size 2, 4, 8
   int cluster_count[3] = {0, 0, 0};
   int cluster_smem[3] = {0, 0, 0}, cluster_threads[3] = {0, 0, 0};
+  int two_cta = 1;            // CTA path: two CTAs per SM when they fit (DDMGNN_TWO_CTA)
   int *d_bad = nullptr, *d_outbad = nullptr, *d_status = nullptr;
   double *d_rin = nullptr, *d_zout = nullptr;  // host-pointer apply staging
   // pcg
@@ -381,6 +382,8 @@ static int refresh_classes(ddmgnn_ctx* c) {
   // DSMEM traffic; profiles/r01_cluster_2cta_configE.jsonl), hence opt-in.
   const char* env = getenv("DDMGNN_CLUSTER");
   const bool use_cluster = !(env && env[0] == '0');
+  const char* env3 = getenv("DDMGNN_TWO_CTA");
+  c->two_cta = !(env3 && env3[0] == '0');
   const char* env2 = getenv("DDMGNN_CLUSTER_2CTA");
   const bool two_cta = env2 && env2[0] == '1';
   const int node0 = gnn_smem_node_bytes(d);
@@ -574,6 +577,7 @@ static cudaError_t enqueue_gnn(ddmgnn_ctx* c, const double* r, int* status, cons
   a.hbuf = c->d_hbuf; a.cbuf = c->d_cbuf; a.qbuf = c->d_qbuf;
   a.bslices = c->d_bslices; a.n_bslices = c->n_bslices;
   a.csubs = c->d_csubs;
+  a.two_cta = c->two_cta;
   for (int j = 0; j < 3; ++j) {
     a.cluster_count[j] = c->cluster_count[j];
     a.cluster_smem[j] = c->cluster_smem[j];

@@ -143,6 +143,7 @@ struct GnnArgs {
   const int2* bslices;  // flat path: (subdomain, slice) of every slice of a big subdomain
   int n_bslices;
   const int* csubs;     // cluster path: subdomains of one cluster-size class
+  int two_cta;           // CTA path: allow two CTAs per SM for small subdomains
   int cluster_count[3];  // subdomains per cluster size 2, 4, 8 (csubs laid out in that order)
   int cluster_smem[3];   // dynamic shared memory per CTA of each cluster-size class
   int cluster_threads[3];  // threads per CTA (448 when two CTAs fit an SM, else kGnnThreads)

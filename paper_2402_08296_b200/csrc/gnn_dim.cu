@@ -1,8 +1,6 @@
 // One latent dimension of the fused GNN kernels per translation unit (compiled
 // with -DGNN_D=<d>; -DGNN_BIG selects the flat path for oversized subdomains):
 // each unit owns its own 64 KB constant bank, and the units compile in parallel.
-#include <cstdlib>
-
 #include "ddmgnn_internal.h"
 
 #ifndef GNN_D
@@ -48,13 +46,9 @@ cudaError_t DDM_NAME(gnn_launch)(int n_ctas, int k_max, size_t smem, const GnnAr
   if (threads < 128) threads = 128;
   // small subdomains: two CTAs per SM when their shared memory fits (registers:
   // 2 x 448 threads x 72 fit the 64K file) — each CTA's warps fill the other's
-  // barrier bubbles.  DDMGNN_TWO_CTA=0 disables.
-  static const bool two_cta = [] {
-    const char* e = getenv("DDMGNN_TWO_CTA");
-    return !(e && e[0] == '0');
-  }();
+  // barrier bubbles.  DDMGNN_TWO_CTA=0 (read when the context is built) disables.
   constexpr int half = kGnnThreads / 2 / 32 * 32;
-  if (!GNN_TC_Q && two_cta && threads > half &&
+  if (!GNN_TC_Q && a.two_cta && threads > half &&
       2 * (smem + sizeof(GnnShared) + 1024) <= 228u * 1024u)
     threads = half;
   gnn_kernel<GNN_D><<<n_ctas, threads, smem, s>>>(a);

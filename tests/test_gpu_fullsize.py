@@ -106,3 +106,23 @@ def test_config_e_cluster_matches_flat(ddm, monkeypatch, ns, cs):
             assert torch.equal(out[path], p(r))
     z1, z0 = out["1"].cpu().numpy(), out["0"].cpu().numpy()
     assert rel_l2(z1, z0) < 1e-6
+
+
+def test_two_ctas_per_sm_matches_oracle(ddm, monkeypatch):
+    """Subdomains small enough for two CTAs per SM (448 threads, several slice
+    rounds per warp) against the oracle and against one CTA per SM."""
+    from oracle import ddm_oracle as orc
+
+    prob = _build(30_000, ns=500, overlap=1)
+    model = ddm.init_model(10, 10, seed=1)
+    r = np.random.default_rng(0).standard_normal(prob.system.n)
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("DDMGNN_TWO_CTA", mode)
+        p = ddm.build_ddm_gnn(prob.system.a, prob.coords, prob.dec, model)
+        assert 448 < p.info()["k_max"] <= 900 and p.info()["n_big"] == 0
+        out[mode] = p(r)
+    om = orc.model_from_flat(10, 10, model.alpha, 2, ddm.flat_params(model))
+    ref = orc.OraclePreconditioner(prob.system.a, prob.coords, prob.dec.subdomains, om, "two")(r)
+    assert rel_l2(out["1"], ref) < TOL
+    assert rel_l2(out["1"], out["0"]) < 1e-6
