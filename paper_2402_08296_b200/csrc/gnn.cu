@@ -4,7 +4,7 @@
 #include "gnn_cfg.h"
 
 #ifndef DDM_GNN_DIMS
-#define DDM_GNN_DIMS(X) X(3) X(4) X(10)
+#define DDM_GNN_DIMS(X) X(3) X(4) X(5) X(10) X(20)
 #endif
 
 namespace ddmgnn {

@@ -241,7 +241,7 @@ int pack_model(int k_bar, int d, double alpha, const double* params, long long n
   int o[kBankOffsets];
   if (!gnn_bank_offsets(d, o)) {
     *err = "latent dimension d=" + std::to_string(d) +
-           " has no compiled kernel (supported: 3, 4, 10)";
+           " has no compiled kernel (supported: 3, 4, 5, 10, 20)";
     return kValueError;
   }
   const long long expect = static_cast<long long>(k_bar) * (11ll * d * d + 15ll * d + 1);

@@ -398,3 +398,20 @@ def test_pcg_ddm_gnn_desk_config_a(ddm):
     ref = g["desk_pcg_hist"]
     assert bool(rep.converged) == bool(g["desk_pcg_converged"])
     assert abs(rep.iterations - (len(ref) - 1)) <= 1
+
+
+@pytest.mark.parametrize("d,k_bar", [(5, 10), (20, 3), (20, 10)])
+def test_other_latent_dims_match_oracle(ddm, d, k_bar):
+    """Latent widths besides d=10 (BASELINE config E's optional d in {5, 20});
+    d=20 with k_bar=10 needs several constant-bank chunks."""
+    from oracle import ddm_oracle as orc
+
+    g = load_golden("A.npz")
+    a, _b, coords, dec = _dec(ddm, g)
+    model = ddm.init_model(k_bar, d, seed=5)
+    om = orc.model_from_flat(k_bar, d, model.alpha, 5, ddm.flat_params(model))
+    for level in ("one", "two"):
+        p = ddm.build_ddm_gnn(a, coords, dec, model, level=level)
+        assert p.info()["d"] == d
+        ref = orc.OraclePreconditioner(a, coords, dec.subdomains, om, level)
+        assert rel_l2(p(g["r"]), ref(g["r"])) < TOL

@@ -1,6 +1,6 @@
 """BASELINE config E: GNN-apply microbench sweep — subdomain size x overlap x
 message-passing depth on synthetic blob meshes (target >= 50 N_s nodes so K >= 50),
-random-init weights, d = 10.  One JSON line per configuration:
+random-init weights, d = 10 (or --dims).  One JSON line per configuration:
 applies timed with CUDA events (L2 flushed), executed FP32 TFLOP/s of the GNN
 launch against the FP32 CUDA-core peak (bench.py's roofline definition).
 
@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--sizes", default="500,1000,2000,5000")
     ap.add_argument("--overlaps", default="1,2,3")
     ap.add_argument("--kbars", default="5,10,20,30")
+    ap.add_argument("--dims", default="10", help="latent widths d (config E: 10, optionally 5, 20)")
     ap.add_argument("--min-nodes", type=int, default=100_000)
     ap.add_argument("--reps", type=int, default=10)
     args = ap.parse_args()
@@ -42,9 +43,10 @@ def main():
             t_build = time.perf_counter() - t0
             r = torch.tensor(np.random.default_rng(0).standard_normal(prob.system.n), device=dev)
             z = torch.empty_like(r)
-            for kb in [int(x) for x in args.kbars.split(",")]:
+            for kb, dd in [(int(x), int(y)) for x in args.kbars.split(",")
+                           for y in args.dims.split(",")]:
                 p = ddm.build_ddm_gnn(prob.system.a, prob.coords, prob.dec,
-                                      ddm.init_model(kb, 10, seed=1))
+                                      ddm.init_model(kb, dd, seed=1))
                 ctx, info = p.context, p.info()
                 for _ in range(2):
                     ctx.apply_device(r.data_ptr(), z.data_ptr(), 2, st.cuda_stream, True)
@@ -67,9 +69,9 @@ def main():
                         torch.cuda.synchronize()
                         dst.append(e0.elapsed_time(e1))
                 gms = float(np.median(tg))
-                fl = gnn_flops_exec(kb, 10, info["V"], info["E"])
+                fl = gnn_flops_exec(kb, dd, info["V"], info["E"])
                 print(json.dumps({
-                    "N_s": ns, "overlap": ov, "k_bar": kb, "N": prob.system.n, "K": info["K"],
+                    "N_s": ns, "overlap": ov, "k_bar": kb, "d": dd, "N": prob.system.n, "K": info["K"],
                     "V": info["V"], "E": info["E"], "k_max": info["k_max"], "n_big": info["n_big"],
                     "apply_ms": float(np.median(ta)), "gnn_ms": gms,
                     "gnn_tflops": fl / (gms * 1e-3) / 1e12,
