@@ -1,6 +1,8 @@
 // One latent dimension of the fused GNN kernels per translation unit (compiled
 // with -DGNN_D=<d>; -DGNN_BIG selects the flat path for oversized subdomains):
 // each unit owns its own 64 KB constant bank, and the units compile in parallel.
+#include <algorithm>
+
 #include "ddmgnn_internal.h"
 
 #ifndef GNN_D
@@ -42,12 +44,13 @@ cudaError_t DDM_NAME(gnn_launch)(int n_ctas, int k_max, size_t smem, const GnnAr
   // tensor-core groups are 4 warps (one per TMEM lane quarter): multiples of 128
   constexpr int gran = GNN_TC_Q ? 128 : 32;
   int threads = ((k_max + gran - 1) / gran) * gran;
-  if (threads > kGnnThreads) threads = kGnnThreads / gran * gran;
+  constexpr int cap = gnn_cta_threads<GNN_D>();
+  if (threads > cap) threads = cap / gran * gran;
   if (threads < 128) threads = 128;
   // small subdomains: two CTAs per SM when their shared memory fits (registers:
   // 2 x 448 threads x 72 fit the 64K file) — each CTA's warps fill the other's
   // barrier bubbles.  DDMGNN_TWO_CTA=0 (read when the context is built) disables.
-  constexpr int half = kGnnThreads / 2 / 32 * 32;
+  constexpr int half = cap / 2 / 32 * 32;
   if (!GNN_TC_Q && a.two_cta && threads > half &&
       2 * (smem + sizeof(GnnShared) + 1024) <= 228u * 1024u)
     threads = half;
@@ -108,7 +111,7 @@ cudaError_t DDM_NAME(gnn_launch)(int n_subs, int /*k_max*/, size_t /*smem*/, con
     off += cnt;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cnt * cs);
-    cfg.blockDim = dim3(a.cluster_threads[j]);
+    cfg.blockDim = dim3(std::min(a.cluster_threads[j], gnn_cta_threads<GNN_D>()));
     cfg.dynamicSmemBytes = a.cluster_smem[j];
     cfg.stream = s;
     cudaLaunchAttribute at[1];

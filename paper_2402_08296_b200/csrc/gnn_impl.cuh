@@ -847,8 +847,14 @@ __device__ __forceinline__ double restrict_sub(const GnnArgs& a, GnnShared& sh, 
 
 // Subdomains whose node state fits the launch's shared memory (k <= a.cap0): one
 // CTA per subdomain (LPT order), the whole chunk of layers on chip.
+// Threads per CTA of the CTA and cluster paths: wide latents (d > 10) carry twice
+// the per-lane state, so they trade warps for registers (512 x 128 instead of
+// 896 x 72) rather than spill.
 template <int D>
-__global__ void __launch_bounds__(kGnnThreads, 1) gnn_kernel(GnnArgs a) {
+constexpr int gnn_cta_threads() { return D > 10 ? 512 : kGnnThreads; }
+
+template <int D>
+__global__ void __launch_bounds__(gnn_cta_threads<D>(), 1) gnn_kernel(GnnArgs a) {
   using C = Cfg<D>;
   if (a.skip != nullptr && uni(*a.skip) != 0) return;
   __shared__ GnnShared sh;
@@ -1069,7 +1075,7 @@ struct ClusterRows {
 };
 
 template <int D>
-__global__ void __launch_bounds__(kGnnThreads, 1) gnn_cluster_kernel(GnnArgs a) {
+__global__ void __launch_bounds__(gnn_cta_threads<D>(), 1) gnn_cluster_kernel(GnnArgs a) {
   using C = Cfg<D>;
   namespace cg = cooperative_groups;
   if (a.skip != nullptr && uni(*a.skip) != 0) return;  // same flag for the whole cluster
