@@ -127,3 +127,25 @@ def test_validate_csr():
     if bad.indptr[4] - bad.indptr[3] > 1:
         with pytest.raises(ValueError, match="row 3"):
             validate_csr(bad)
+
+
+def test_gnn_launch_count():
+    """Launches per GNN forward as bench.py reports them (gpu_launches): per chunk
+    the CTA kernel (if any subdomain fits one CTA), one per cluster size in use,
+    and for flat-path subdomains a restriction prologue (first chunk) + 2 per layer."""
+    from paper_2402_08296_b200._lib import Context
+
+    ctx = Context.__new__(Context)
+
+    def count(**kw):
+        base = dict(K=997, n_big=0, n_cluster=0, cluster_launches=0, k_bar=10, lmax=10,
+                    n_chunks=1)
+        base.update(kw)
+        ctx.info = lambda: base
+        return ctx.gnn_launches()
+
+    assert count() == 1
+    assert count(n_big=7, n_cluster=7, cluster_launches=1) == 2          # config C
+    assert count(K=50, n_big=50, n_cluster=50, cluster_launches=2) == 2  # clusters only
+    assert count(n_big=3, n_cluster=0) == 1 + 1 + 20                     # flat path
+    assert count(k_bar=30, n_chunks=3, n_big=2, n_cluster=1, cluster_launches=1) == 3 * 2 + 1 + 60
