@@ -52,6 +52,9 @@ typedef struct ddmgnn_ctx ddmgnn_ctx;
 #define DDMGNN_ASM_ONE 3      /* DDM-LU comparator: exact local solves (asm.py:84-113, "ddm-lu-1") */
 #define DDMGNN_ASM_TWO 4      /* DDM-LU two-level (cli.py:69-70, "ddm-lu-2") */
 #define DDMGNN_IC0 5          /* IC(0) comparator (sparse.py:170-227, "ic0") */
+/* OR into the level of ddmgnn_pcg: flexible CG (Polak-Ribiere beta = <r, z - z_old> / rho
+ * instead of the reference's rho'/rho at sparse.py:124; opt-in, not in the reference). */
+#define DDMGNN_FLEXIBLE 0x100
 
 const char* ddmgnn_last_error(void);
 int ddmgnn_version(void);
@@ -106,16 +109,25 @@ int ddmgnn_apply(ddmgnn_ctx* ctx, const double* r_dev, double* z_dev, int level,
                  int check);
 /* Same with host pointers: H2D copy, apply, D2H copy (end-to-end path). */
 int ddmgnn_apply_host(ddmgnn_ctx* ctx, const double* r, double* z, int level);
-/* Launch only the fused restriction + GNN kernel(s) on r_dev (profiling aid). */
+/* Launch only the fused restriction + GNN kernel(s) on r_dev (sharded building block,
+ * profiling aid).  Asynchronous; non-finite model states are recorded in the context's
+ * status word (see ddmgnn_apply_status). */
 int ddmgnn_launch_gnn_only(ddmgnn_ctx* ctx, const double* r_dev, void* stream);
+/* Synchronise `stream` and report a non-finite model state recorded by the launches
+ * since the last check with the reference's message ("non-finite latent state at
+ * message-passing iteration k" / "non-finite model output in subdomain i"; local
+ * subdomain indices); clears the status word. */
+int ddmgnn_apply_status(ddmgnn_ctx* ctx, void* stream);
 /* y = A x on device pointers. */
 int ddmgnn_spmv(ddmgnn_ctx* ctx, const double* x_dev, double* y_dev, void* stream);
 
 /* Device-resident PCG (sparse.py:76-127) with the GNN preconditioner at `level`
  * (or plain CG for DDMGNN_PRECOND_NONE).  b, u0 (may be NULL), u are host pointers
  * when device_ptrs == 0 and device pointers otherwise; history must hold
- * max_iter + 1 doubles (host).  On return *iterations, history[0..*iterations],
- * *converged are filled exactly like SolveReport (sparse.py:31-53). */
+ * max_iter + 1 doubles (host; 1 when max_iter <= 0 — a negative max_iter runs no
+ * iteration, like the reference).  On return *iterations, history[0..*iterations],
+ * *converged are filled exactly like SolveReport (sparse.py:31-53).
+ * level | DDMGNN_FLEXIBLE selects the opt-in flexible CG. */
 int ddmgnn_pcg(ddmgnn_ctx* ctx, const double* b, const double* u0, double* u, double tol,
                int max_iter, int level, int device_ptrs, void* stream, int* iterations,
                double* history, int* converged);
@@ -124,8 +136,8 @@ int ddmgnn_pcg(ddmgnn_ctx* ctx, const double* b, const double* u0, double* u, do
  * the Krylov recurrence still runs on the device.  The callback returns 0 on success. */
 typedef int (*ddmgnn_host_precond_fn)(void* user, const double* r, double* z, int64_t n);
 int ddmgnn_pcg_host_precond(ddmgnn_ctx* ctx, const double* b, const double* u0, double* u,
-                            double tol, int max_iter, ddmgnn_host_precond_fn fn, void* user,
-                            int* iterations, double* history, int* converged);
+                            double tol, int max_iter, int flexible, ddmgnn_host_precond_fn fn,
+                            void* user, int* iterations, double* history, int* converged);
 
 /* ---- Sharded solve building blocks (one process per GPU) ----
  * A rank's context holds its group of subdomains over its local DOF set; the
@@ -145,16 +157,20 @@ int ddmgnn_scatter(const double* src, const int32_t* idx, int64_t n, double* dst
 /* *out = x . y (fixed two-stage order; work holds >= 1184 doubles). */
 int ddmgnn_dot(int64_t n, const double* x, const double* y, double* work, double* out,
                void* stream);
+/* *out = x . (y - w) (same order as ddmgnn_dot; the flexible-CG numerator <r, z - z_old>). */
+int ddmgnn_dot_diff(int64_t n, const double* x, const double* y, const double* w, double* work,
+                    double* out, void* stream);
 /* u += alpha p, r -= alpha q (sparse.py:112-113), *rr_out = r . r (sparse.py:114). */
 int ddmgnn_axpy2(int64_t n, double alpha, const double* p, const double* q, double* u, double* r,
                  double* work, double* rr_out, void* stream);
 /* p = z + beta p (sparse.py:126). */
 int ddmgnn_xpby(int64_t n, const double* z, double beta, double* p, void* stream);
 /* Device-side scalars of the distributed PCG: st = {rho, pq, alpha, rr, nb, tol, rz,
- * beta, iter, status, max_iter} (fp64, device).  op 0: alpha = rho / pq (status 3 if
+ * beta, iter, status, max_iter, rzo} (fp64, device).  op 0: alpha = rho / pq (status 3 if
  * pq <= 0, sparse.py:108-111); op 1: rel = sqrt(rr) / nb, hist[++iter] = rel, status
  * 1 converged / 2 max_iter / 4 non-finite (sparse.py:114-121); op 2: beta = rz / rho,
- * rho = rz (sparse.py:123-125).  No-ops once status != 0. */
+ * rho = rz (sparse.py:123-125); op 3 (flexible CG): beta = rzo / rho, rho = rz.
+ * No-ops once status != 0. */
 int ddmgnn_pcg_scalars(int op, double* st, double* hist, void* stream);
 /* ddmgnn_axpy2 / ddmgnn_xpby with alpha / beta read from st (no-ops once status != 0). */
 int ddmgnn_axpy2_dev(int64_t n, const double* st, const double* p, const double* q, double* u,

@@ -294,8 +294,14 @@ def plan_batches(node_counts, cap: int):
 # PCG (sparse.py:76-127)
 
 
-def pcg(a, b, precond, tol: float, max_iter: int, u0=None):
-    """Returns (u, iterations, history, converged)."""
+def pcg(a, b, precond, tol: float, max_iter: int, u0=None, flexible: bool = False):
+    """Returns (u, iterations, history, converged).
+
+    ``flexible=True`` is the opt-in flexible CG (Polak-Ribiere beta,
+    beta = <r_k+1, z_k+1 - z_k> / <r_k, z_k>; Notay 2000) that the
+    reference does NOT have (SURVEY.md finding 3): the SURVEY's flexible-CG
+    probe recipe (appendix).  Every other line is sparse.py:76-127; with a
+    linear SPD preconditioner it equals PCG in exact arithmetic."""
     if tol <= 0:
         raise ValueError("tol must be positive")
     b = np.asarray(b, dtype=float)
@@ -329,9 +335,10 @@ def pcg(a, b, precond, tol: float, max_iter: int, u0=None):
         if rel < tol:
             converged = True
             break
+        z_old = z
         z = precond(r) if precond is not None else r
         rho_next = float(r @ z)
-        beta = rho_next / rho
+        beta = (float(r @ (z - z_old)) if flexible else rho_next) / rho
         rho = rho_next
         p = z + beta * p
     return u, iterations, history, converged

@@ -11,7 +11,7 @@ from .decomp import Decomposition, extend, finish_decomposition, nicolaides, res
 from .dss import (DssModel, IterationWeights, Mlp, flat_params, init_model, load_model,
                   param_arrays, param_count, save_model)
 from .hybrid import DdmGnnPreconditioner, apply_ddm_gnn, build_ddm_gnn, plan_batches
-from .sparse import Ic0Preconditioner, SolveReport, cg, ic0, pcg, validate_csr
+from .sparse import Ic0Preconditioner, SolveReport, cg, fcg, ic0, pcg, validate_csr
 
 __version__ = "0.1.0"
 
@@ -20,6 +20,6 @@ __all__ = [
     "DssModel", "IterationWeights", "Mlp", "init_model", "load_model", "save_model",
     "param_count", "param_arrays", "flat_params",
     "DdmGnnPreconditioner", "build_ddm_gnn", "apply_ddm_gnn", "plan_batches",
-    "SolveReport", "pcg", "cg", "validate_csr", "AsmPreconditioner", "build_asm", "apply_asm",
+    "SolveReport", "pcg", "fcg", "cg", "validate_csr", "AsmPreconditioner", "build_asm", "apply_asm",
     "Ic0Preconditioner", "ic0",
 ]

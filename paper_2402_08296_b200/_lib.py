@@ -24,6 +24,7 @@ LEVEL_TWO = 2
 ASM_ONE = 3
 ASM_TWO = 4
 IC0 = 5
+FLEXIBLE = 0x100  # OR into the pcg level: opt-in flexible CG (Polak-Ribiere beta)
 LEGACY_STREAM = 1  # cudaStreamLegacy
 
 _i64 = ctypes.c_int64
@@ -62,16 +63,18 @@ SIGNATURES = [
     ("ddmgnn_apply", _int, [_ctx, _vp, _vp, _int, _vp, _int]),
     ("ddmgnn_apply_host", _int, [_ctx, _pd, _pd, _int]),
     ("ddmgnn_launch_gnn_only", _int, [_ctx, _vp, _vp]),
+    ("ddmgnn_apply_status", _int, [_ctx, _vp]),
     ("ddmgnn_spmv", _int, [_ctx, _vp, _vp, _vp]),
     ("ddmgnn_pcg", _int, [_ctx, _vp, _vp, _vp, _dbl, _int, _int, _int, _vp, _pint, _pd, _pint]),
     ("ddmgnn_pcg_host_precond", _int,
-     [_ctx, _pd, _pd, _pd, _dbl, _int, HOST_PRECOND_FN, _vp, _pint, _pd, _pint]),
+     [_ctx, _pd, _pd, _pd, _dbl, _int, _int, HOST_PRECOND_FN, _vp, _pint, _pd, _pint]),
     ("ddmgnn_local_outputs", _int, [_ctx, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
                                     ctypes.POINTER(_vp)]),
     ("ddmgnn_set_pou", _int, [_ctx, _i64, _pd]),
     ("ddmgnn_gather", _int, [_vp, _vp, _i64, _vp, _vp]),
     ("ddmgnn_scatter", _int, [_vp, _vp, _i64, _vp, _vp]),
     ("ddmgnn_dot", _int, [_i64, _vp, _vp, _vp, _vp, _vp]),
+    ("ddmgnn_dot_diff", _int, [_i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     ("ddmgnn_axpy2", _int, [_i64, _dbl, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     ("ddmgnn_xpby", _int, [_i64, _vp, _dbl, _vp, _vp]),
     ("ddmgnn_dense_gemv", _int, [_i64, _vp, _vp, _vp, _vp]),
@@ -252,6 +255,11 @@ class Context:
     def launch_gnn_only(self, r_ptr: int, stream: int = 0):
         check(self._lib.ddmgnn_launch_gnn_only(self._h, _vp(r_ptr), _vp(stream or None)))
 
+    def apply_status(self, stream: int = 0):
+        """Raise the reference's error if a launch since the last check saw a
+        non-finite model state (synchronises the stream)."""
+        check(self._lib.ddmgnn_apply_status(self._h, _vp(stream or None)))
+
     def set_pou(self, pou):
         w = np.ascontiguousarray(pou, dtype=np.float64)
         check(self._lib.ddmgnn_set_pou(self._h, w.size, dptr(w)))
@@ -266,11 +274,14 @@ class Context:
     def spmv_device(self, x_ptr: int, y_ptr: int, stream: int = 0):
         check(self._lib.ddmgnn_spmv(self._h, _vp(x_ptr), _vp(y_ptr), _vp(stream or None)))
 
-    def pcg(self, b, u0, tol, max_iter, level, device_ptrs=False, u_out=None, stream=0):
+    def pcg(self, b, u0, tol, max_iter, level, device_ptrs=False, u_out=None, stream=0,
+            flexible=False):
         """Returns (u, iterations, history, converged)."""
         it = ctypes.c_int(0)
         conv = ctypes.c_int(0)
-        hist = np.zeros(max_iter + 1, dtype=np.float64)
+        hist = np.zeros(max(0, max_iter) + 1, dtype=np.float64)
+        if flexible:
+            level = int(level) | FLEXIBLE
         if device_ptrs:
             status = self._lib.ddmgnn_pcg(self._h, _vp(b), _vp(u0 or None), _vp(u_out), float(tol),
                                           int(max_iter), int(level), 1, _vp(stream or None),
@@ -288,7 +299,7 @@ class Context:
         check(status)
         return u, it.value, hist[: it.value + 1].tolist(), bool(conv.value)
 
-    def pcg_host_precond(self, b, u0, tol, max_iter, fn):
+    def pcg_host_precond(self, b, u0, tol, max_iter, fn, flexible=False):
         b = np.ascontiguousarray(b, dtype=np.float64)
         n = b.shape[0]
         u = np.empty_like(b)
@@ -310,10 +321,11 @@ class Context:
         cfn = HOST_PRECOND_FN(cb)
         it = ctypes.c_int(0)
         conv = ctypes.c_int(0)
-        hist = np.zeros(max_iter + 1, dtype=np.float64)
+        hist = np.zeros(max(0, max_iter) + 1, dtype=np.float64)
         status = self._lib.ddmgnn_pcg_host_precond(
             self._h, dptr(b), None if u0a is None else dptr(u0a), dptr(u), float(tol),
-            int(max_iter), cfn, None, ctypes.byref(it), dptr(hist), ctypes.byref(conv))
+            int(max_iter), int(bool(flexible)), cfn, None, ctypes.byref(it), dptr(hist),
+            ctypes.byref(conv))
         if err:
             raise err[0]
         check(status)

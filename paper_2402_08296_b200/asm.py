@@ -14,6 +14,7 @@ import scipy.linalg
 import scipy.sparse as sp
 
 from .decomp import Decomposition
+from .sparse import private_copy
 
 __all__ = ["extract_local_matrix", "coarse_matrix", "coarse_inverse", "AsmPreconditioner",
            "build_asm", "apply_asm"]
@@ -183,7 +184,7 @@ def build_asm(a: sp.csr_matrix, dec: Decomposition, level: str, device: int = 0,
             raise RuntimeError(msg if msg.startswith("singular coarse matrix")
                                else f"singular coarse matrix: {msg}") from exc
         ctx.set_coarse_inverse(cinv)
-    return AsmPreconditioner(ctx, a, dec, level, cm)
+    return AsmPreconditioner(ctx, private_copy(a), dec, level, cm)
 
 
 def apply_asm(p: AsmPreconditioner, r):

@@ -121,7 +121,9 @@ struct ddmgnn_ctx {
   PcgState* d_st = nullptr;
   PcgState* h_st = nullptr;  // pinned
   double *h_pin_a = nullptr, *h_pin_b = nullptr;  // pinned staging (n doubles each)
-  cudaGraphExec_t graph_exec[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  cudaGraphExec_t graph_exec[12] = {};  // [level + 6 * flexible]
+  int pcg_flex = 0;            // flexible CG in the PCG being enqueued / captured
+  double* d_zold = nullptr;    // flexible CG: previous z (IC(0) / host-callback paths)
   // DDM-LU comparator: dense local inverses (row-major, offsets in doubles)
   double* d_ainv = nullptr;
   long long* d_ainv_off = nullptr;
@@ -210,7 +212,7 @@ extern "C" void ddmgnn_destroy(ddmgnn_ctx* c) {
   dfree(c->d_bank); dfree(c->d_cinv); dfree(c->d_status);
   dfree(c->d_rin); dfree(c->d_zout);
   dfree(c->d_b); dfree(c->d_u); dfree(c->d_r); dfree(c->d_p); dfree(c->d_q); dfree(c->d_z);
-  dfree(c->d_partials); dfree(c->d_hist); dfree(c->d_st);
+  dfree(c->d_partials); dfree(c->d_hist); dfree(c->d_st); dfree(c->d_zold);
   if (c->h_st) cudaFreeHost(c->h_st);
   if (c->h_pin_a) cudaFreeHost(c->h_pin_a);
   if (c->h_pin_b) cudaFreeHost(c->h_pin_b);
@@ -288,6 +290,7 @@ extern "C" int ddmgnn_set_matrix(ddmgnn_ctx* c, int64_t n, int64_t nnz, const in
   CUDA_TRY(dalloc(&c->d_b, n)); CUDA_TRY(dalloc(&c->d_u, n)); CUDA_TRY(dalloc(&c->d_r, n));
   CUDA_TRY(dalloc(&c->d_p, n)); CUDA_TRY(dalloc(&c->d_q, n)); CUDA_TRY(dalloc(&c->d_z, n));
   CUDA_TRY(dalloc(&c->d_rin, n)); CUDA_TRY(dalloc(&c->d_zout, n));
+  dfree(c->d_zold);  // flexible CG scratch, reallocated at the new size on demand
   const int pblocks = std::max((static_cast<int>(n) + 255) / 256, 148 * 8) + 1;
   CUDA_TRY(dalloc(&c->d_partials, 2ull * pblocks));
   if (!c->d_st) {
@@ -565,8 +568,70 @@ static int ready(ddmgnn_ctx* c, int level) {
   return kOk;
 }
 
+// ---- the GNN weight bank is process-global device state ----
+// The fused GNN kernels read their weights from a __constant__ bank per compiled
+// latent width (gnn_dim.cu), which every apply re-fills on its stream before the
+// launch.  Two applies on different streams (two contexts, or one context used from
+// two streams) must therefore not overlap: every bank use is chained behind the
+// previous one on the device by an event whenever the stream changes.  The host
+// mutex keeps upload + launch + record of one use together.
+namespace {
+struct BankChain {
+  std::mutex m;
+  cudaEvent_t ev = nullptr;
+  cudaStream_t last = nullptr;
+  bool valid = false;
+};
+BankChain g_bank[64];
+
+class BankUse {
+ public:
+  BankUse(int device, cudaStream_t s) : s_(s) {
+    g_ = (device >= 0 && device < 64) ? &g_bank[device] : nullptr;
+    if (!g_) return;
+    lk_ = std::unique_lock<std::mutex>(g_->m);
+    if (!g_->ev) err_ = cudaEventCreateWithFlags(&g_->ev, cudaEventDisableTiming);
+    if (err_ == cudaSuccess && g_->valid && g_->last != s) err_ = cudaStreamWaitEvent(s, g_->ev, 0);
+  }
+  cudaError_t error() const { return err_; }
+  // call after the last bank-reading launch has been enqueued on s
+  cudaError_t done() {
+    if (!g_ || err_ != cudaSuccess) return err_;
+    err_ = cudaEventRecord(g_->ev, s_);
+    g_->last = s_;
+    g_->valid = err_ == cudaSuccess;
+    return err_;
+  }
+
+ private:
+  BankChain* g_ = nullptr;
+  cudaStream_t s_;
+  std::unique_lock<std::mutex> lk_;
+  cudaError_t err_ = cudaSuccess;
+};
+
+bool capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
+}
+}  // namespace
+
+static cudaError_t enqueue_gnn_impl(ddmgnn_ctx* c, const double* r, int* status, const int* skip,
+                                    cudaStream_t s);
+
 // Enqueue restriction + GNN chunks.  status/skip: apply error word and PCG skip word.
+// Under stream capture (PCG graph) the chain is kept around the graph launches instead.
 static cudaError_t enqueue_gnn(ddmgnn_ctx* c, const double* r, int* status, const int* skip,
+                               cudaStream_t s) {
+  if (capturing(s)) return enqueue_gnn_impl(c, r, status, skip, s);
+  BankUse use(c->device, s);
+  if (use.error() != cudaSuccess) return use.error();
+  cudaError_t e = enqueue_gnn_impl(c, r, status, skip, s);
+  if (e != cudaSuccess) return e;
+  return use.done();
+}
+
+static cudaError_t enqueue_gnn_impl(ddmgnn_ctx* c, const double* r, int* status, const int* skip,
                                cudaStream_t s) {
   const DeviceLayout& L = c->lay;
   const PackedModel& M = c->model;
@@ -612,9 +677,14 @@ static cudaError_t enqueue_apply(ddmgnn_ctx* c, const double* r, double* z, int 
   const bool two = level == DDMGNN_LEVEL_TWO || level == DDMGNN_ASM_TWO;
   cudaError_t e;
   if (level == DDMGNN_IC0) {  // z = L^-T (L^-1 r)  (sparse.py:177-179)
+    const bool flex = mode == 1 && c->pcg_flex;
+    if (flex) {
+      e = cudaMemcpyAsync(c->d_zold, z, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) return e;
+    }
     e = launch_ic0_apply(c->ic0, r, c->d_ic_tmp, z, skip, s);
     if (e != cudaSuccess || mode != 1) return e;
-    return launch_rz_beta(c->n, r, z, c->d_partials, c->d_st, s);
+    return launch_rz_beta(c->n, r, z, flex ? c->d_zold : nullptr, c->d_partials, c->d_st, s);
   }
   if (asm_) {
     e = launch_asm_local(c->K, c->lay.k_max, c->lay.sub_ptr, c->lay.idx, c->d_ainv_off,
@@ -738,6 +808,12 @@ extern "C" int ddmgnn_launch_gnn_only(ddmgnn_ctx* c, const double* r, void* stre
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(enqueue_gnn(c, r, c->d_status, nullptr, pick(c, stream)));
   return kOk;
+}
+
+extern "C" int ddmgnn_apply_status(ddmgnn_ctx* c, void* stream) {
+  if (!c || !c->built) return fail(kStateError, "build must be called first");
+  CUDA_TRY(cudaSetDevice(c->device));
+  return check_status_word(c, pick(c, stream));
 }
 
 extern "C" int ddmgnn_set_ic0(ddmgnn_ctx* c) {
@@ -867,18 +943,19 @@ static cudaError_t enqueue_iteration(ddmgnn_ctx* c, int level, cudaStream_t s) {
 }
 
 static int get_graph(ddmgnn_ctx* c, int level, cudaGraphExec_t* out) {
-  if (!c->graph_exec[level]) {
+  const int slot = level + 6 * (c->pcg_flex ? 1 : 0);
+  if (!c->graph_exec[slot]) {
     cudaGraph_t g;
     CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     cudaError_t e = enqueue_iteration(c, level, c->stream);
     cudaError_t e2 = cudaStreamEndCapture(c->stream, &g);
     if (e != cudaSuccess) return fail(kCudaError, std::string("graph capture: ") + cudaGetErrorString(e));
     if (e2 != cudaSuccess) return fail(kCudaError, std::string("graph capture: ") + cudaGetErrorString(e2));
-    e = cudaGraphInstantiate(&c->graph_exec[level], g, 0);
+    e = cudaGraphInstantiate(&c->graph_exec[slot], g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return fail(kCudaError, std::string("graph instantiate: ") + cudaGetErrorString(e));
   }
-  *out = c->graph_exec[level];
+  *out = c->graph_exec[slot];
   return kOk;
 }
 
@@ -905,6 +982,8 @@ static int pcg_prologue(ddmgnn_ctx* c, const double* b, const double* u0, int de
   PcgState init{};
   init.tol = tol;
   init.max_iter = max_iter;
+  init.flexible = c->pcg_flex;
+  if (c->pcg_flex && !c->d_zold) CUDA_TRY(dalloc(&c->d_zold, n));
   *c->h_st = init;
   CUDA_TRY(cudaMemcpyAsync(c->d_st, c->h_st, sizeof(PcgState), cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaMemcpyAsync(c->d_b, b, bytes, kin, s));
@@ -966,12 +1045,17 @@ static int pcg_epilogue(ddmgnn_ctx* c, int device_ptrs, cudaStream_t s, double* 
 extern "C" int ddmgnn_pcg(ddmgnn_ctx* c, const double* b, const double* u0, double* u, double tol,
                           int max_iter, int level, int device_ptrs, void* stream, int* iterations,
                           double* history, int* converged) {
+  if (!c) return fail(kValueError, "null context");
+  const int flex = (level & DDMGNN_FLEXIBLE) ? 1 : 0;
+  level &= ~DDMGNN_FLEXIBLE;
   int st = ready(c, level);
   if (st) return st;
   if (!(tol > 0)) return fail(kValueError, "tol must be positive");
-  if (max_iter < 0) return fail(kValueError, "max_iter must be >= 0");
+  // the reference's loop simply does not run for max_iter < 0 (sparse.py:105)
+  if (max_iter < 0) max_iter = 0;
   CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t s = pick(c, stream);
+  c->pcg_flex = flex;
   int early = 0;
   st = pcg_prologue(c, b, u0, device_ptrs, tol, max_iter, s, &early, iterations, history,
                     converged, u);
@@ -991,9 +1075,19 @@ extern "C" int ddmgnn_pcg(ddmgnn_ctx* c, const double* b, const double* u0, doub
     cudaGraphExec_t gx;
     st = get_graph(c, level, &gx);
     if (st) return st;
+    const bool gnn = level == DDMGNN_LEVEL_ONE || level == DDMGNN_LEVEL_TWO;
     int done = 0, chunk = 2;
     while (!done) {
-      for (int t = 0; t < chunk; ++t) CUDA_TRY(cudaGraphLaunch(gx, s));
+      for (int t = 0; t < chunk; ++t) {
+        if (gnn) {  // the captured iteration re-fills the weight bank (see BankUse)
+          BankUse use(c->device, s);
+          CUDA_TRY(use.error());
+          CUDA_TRY(cudaGraphLaunch(gx, s));
+          CUDA_TRY(use.done());
+        } else {
+          CUDA_TRY(cudaGraphLaunch(gx, s));
+        }
+      }
       CUDA_TRY(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
       CUDA_TRY(cudaStreamSynchronize(s));
       done = c->h_st->status != kRunning;
@@ -1015,15 +1109,17 @@ extern "C" int ddmgnn_pcg(ddmgnn_ctx* c, const double* b, const double* u0, doub
 }
 
 extern "C" int ddmgnn_pcg_host_precond(ddmgnn_ctx* c, const double* b, const double* u0,
-                                       double* u, double tol, int max_iter,
+                                       double* u, double tol, int max_iter, int flexible,
                                        ddmgnn_host_precond_fn fn, void* user, int* iterations,
                                        double* history, int* converged) {
   int st = ready(c, DDMGNN_PRECOND_NONE);
   if (st) return st;
   if (!(tol > 0)) return fail(kValueError, "tol must be positive");
   if (!fn) return fail(kValueError, "null preconditioner callback");
+  if (max_iter < 0) max_iter = 0;  // sparse.py:105: the loop does not run
   CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t s = c->stream;
+  c->pcg_flex = flexible ? 1 : 0;
   int early = 0;
   st = pcg_prologue(c, b, u0, 0, tol, max_iter, s, &early, iterations, history, converged, u);
   if (st || early) return st;
@@ -1054,10 +1150,13 @@ extern "C" int ddmgnn_pcg_host_precond(ddmgnn_ctx* c, const double* b, const dou
     CUDA_TRY(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(PcgState), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     if (c->h_st->status != kRunning) break;
+    if (c->pcg_flex)
+      CUDA_TRY(cudaMemcpyAsync(c->d_zold, c->d_z, bytes, cudaMemcpyDeviceToDevice, s));
     st = host_apply();
     if (st) return st;
     // rho' = <r, z>, beta, p = z + beta p via the prolong-free path
-    CUDA_TRY(launch_rz_beta(n, c->d_r, c->d_z, c->d_partials, c->d_st, s));
+    CUDA_TRY(launch_rz_beta(n, c->d_r, c->d_z, c->pcg_flex ? c->d_zold : nullptr, c->d_partials,
+                            c->d_st, s));
     CUDA_TRY(launch_pupdate(n, c->d_p, c->d_z, c->d_st, s));
   }
   return pcg_epilogue(c, 0, s, u, iterations, history, converged);

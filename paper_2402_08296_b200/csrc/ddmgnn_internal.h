@@ -166,6 +166,10 @@ struct PcgState {
   double rho, pq, alpha, beta, rr, nb, rz, tol;
   int iter, max_iter, status, pad;
   unsigned int tickets[8];
+  // flexible CG (opt-in, not in the reference): beta = <r, z - z_old> / rho
+  double rzo;    // last <r, z - z_old>
+  int flexible;  // 0 = the reference's beta = rho'/rho (sparse.py:124), 1 = Polak-Ribiere
+  int pad2;
 };
 constexpr int kRedThreads = 256;
 int reduce_blocks(int n);
@@ -199,8 +203,9 @@ cudaError_t launch_pcg_init(int n, const double* b, double* r, double* partials,
 cudaError_t launch_rz_init(int n, const double* r, const double* z, double* p, double* partials,
                            PcgState* st, cudaStream_t s);
 cudaError_t launch_copy(int n, const double* src, double* dst, cudaStream_t s);
-cudaError_t launch_rz_beta(int n, const double* r, const double* z, double* partials,
-                           PcgState* st, cudaStream_t s);
+// zold (may be null unless st->flexible): previous z for the flexible beta
+cudaError_t launch_rz_beta(int n, const double* r, const double* z, const double* zold,
+                           double* partials, PcgState* st, cudaStream_t s);
 cudaError_t launch_pcg_init_u0(int n, const double* b, const double* au0, double* r,
                                double* partials, PcgState* st, double* hist, cudaStream_t s);
 

@@ -171,15 +171,19 @@ __global__ void __launch_bounds__(kRedThreads) update_kernel(int n, double* __re
                                                              double* hist, int identity) {
   if (st->status != kRunning) return;
   const double alpha = st->alpha;
-  double rr = 0.0;
+  // plain flexible CG (z = r): beta = <r', r' - r> / rho needs <r', r>
+  const bool flex_id = identity && st->flexible;
+  double rr = 0.0, rro = 0.0;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     u[j] = __dadd_rn(u[j], __dmul_rn(alpha, p[j]));  // sparse.py:112
-    const double rj = __dsub_rn(r[j], __dmul_rn(alpha, q[j]));  // sparse.py:113
+    const double r_old = r[j];
+    const double rj = __dsub_rn(r_old, __dmul_rn(alpha, q[j]));  // sparse.py:113
     r[j] = rj;
     rr += rj * rj;
+    if (flex_id) rro += rj * __dsub_rn(rj, r_old);
   }
-  double v[1] = {rr};
-  if (grid_sum<1>(v, partials, &st->tickets[1])) {
+  double v[2] = {rr, rro};
+  if (grid_sum<2>(v, partials, &st->tickets[1])) {
     const double rel = sqrt(v[0]) / st->nb;  // sparse.py:114
     st->rr = v[0];
     if (!isfinite(rel)) {  // sparse.py:115-116
@@ -194,7 +198,8 @@ __global__ void __launch_bounds__(kRedThreads) update_kernel(int n, double* __re
     } else if (it >= st->max_iter) {
       st->status = kMaxIter;
     } else if (identity) {  // plain CG: z = r, rho' = r.r (sparse.py:122-125)
-      st->beta = v[0] / st->rho;
+      st->rzo = v[1];
+      st->beta = (st->flexible ? v[1] : v[0]) / st->rho;
       st->rho = v[0];
     }
   }
@@ -285,24 +290,31 @@ cudaError_t launch_rz_init(int n, const double* r, const double* z, double* p, d
 
 // rho' = <r, z>, beta = rho'/rho, rho = rho'  (sparse.py:123-125), for host-side
 // preconditioner callbacks
+// (flexible: beta = <r, z - zold> / rho)
 __global__ void __launch_bounds__(kRedThreads) rz_beta_kernel(int n, const double* __restrict__ r,
                                                               const double* __restrict__ z,
+                                                              const double* __restrict__ zold,
                                                               double* partials, PcgState* st) {
   if (st->status != kRunning) return;
-  double rz = 0.0;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
-    rz += r[j] * z[j];
-  double v[1] = {rz};
-  if (grid_sum<1>(v, partials, &st->tickets[5])) {
+  const bool flex = st->flexible && zold != nullptr;
+  double rz = 0.0, rzo = 0.0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const double rj = r[j], zj = z[j];
+    rz += rj * zj;
+    if (flex) rzo += rj * __dsub_rn(zj, zold[j]);
+  }
+  double v[2] = {rz, rzo};
+  if (grid_sum<2>(v, partials, &st->tickets[5])) {
     st->rz = v[0];
-    st->beta = v[0] / st->rho;
+    st->rzo = v[1];
+    st->beta = (flex ? v[1] : v[0]) / st->rho;
     st->rho = v[0];
   }
 }
 
-cudaError_t launch_rz_beta(int n, const double* r, const double* z, double* partials,
-                           PcgState* st, cudaStream_t s) {
-  rz_beta_kernel<<<reduce_blocks(n), kRedThreads, 0, s>>>(n, r, z, partials, st);
+cudaError_t launch_rz_beta(int n, const double* r, const double* z, const double* zold,
+                           double* partials, PcgState* st, cudaStream_t s) {
+  rz_beta_kernel<<<reduce_blocks(n), kRedThreads, 0, s>>>(n, r, z, zold, partials, st);
   return cudaGetLastError();
 }
 
@@ -432,11 +444,12 @@ cudaError_t launch_asm_local(int K, int k_max, const int* sub_ptr, const int* id
 __global__ void __launch_bounds__(kRedThreads) prolong_kernel(
     int n, int two_level, const int* __restrict__ tptr, const int2* __restrict__ tent,
     const double* __restrict__ pou, const double* __restrict__ y,
-    const double* __restrict__ scale, const double* __restrict__ zloc, double* __restrict__ z,
+    const double* __restrict__ scale, const double* __restrict__ zloc, double* z,
     const double* __restrict__ r, double* partials, PcgState* st, int mode,
     const int* skip) {
   if (skip != nullptr && *skip != kRunning) return;
-  double rz = 0.0;
+  const bool flex = mode == 1 && st->flexible;
+  double rz = 0.0, rzo = 0.0;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const int b = tptr[j], e = tptr[j + 1];
     double acc = 0.0;
@@ -459,14 +472,20 @@ __global__ void __launch_bounds__(kRedThreads) prolong_kernel(
         if (scale[pe.y] != 0.0) acc = __dadd_rn(acc, zloc[pe.x]);
       }
     }
+    if (mode == 1) {
+      const double rj = r[j];
+      rz += rj * acc;
+      // flexible CG: z still holds z_old here (z is updated in place)
+      if (flex) rzo += rj * __dsub_rn(acc, z[j]);
+    }
     z[j] = acc;
-    if (mode == 1) rz += r[j] * acc;
   }
   if (mode == 1) {
-    double v[1] = {rz};
-    if (grid_sum<1>(v, partials, &st->tickets[4])) {
+    double v[2] = {rz, rzo};
+    if (grid_sum<2>(v, partials, &st->tickets[4])) {
       st->rz = v[0];
-      st->beta = v[0] / st->rho;  // sparse.py:124
+      st->rzo = v[1];
+      st->beta = (flex ? v[1] : v[0]) / st->rho;  // sparse.py:124 (or Polak-Ribiere)
       st->rho = v[0];
     }
   }

@@ -74,6 +74,18 @@ __global__ void dot_partial_kernel(long long n, const double* __restrict__ x,
   if (threadIdx.x == 0) part[blockIdx.x] = acc;
 }
 
+// partial[b] = sum over the block's grid-stride elements of x*(y - w)  (flexible CG)
+__global__ void dot_diff_partial_kernel(long long n, const double* __restrict__ x,
+                                        const double* __restrict__ y,
+                                        const double* __restrict__ w, double* __restrict__ part) {
+  double acc = 0.0;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    acc += x[i] * __dsub_rn(y[i], w[i]);
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
 __global__ void sum_partials_kernel(int nb, const double* __restrict__ part,
                                     double* __restrict__ out) {
   double acc = 0.0;
@@ -137,6 +149,15 @@ extern "C" int ddmgnn_dot(int64_t n, const double* x, const double* y, double* w
   return cuda_status(cudaGetLastError());
 }
 
+extern "C" int ddmgnn_dot_diff(int64_t n, const double* x, const double* y, const double* w,
+                               double* work, double* out, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int nb = nblocks(n);
+  dot_diff_partial_kernel<<<nb, kT, 0, s>>>(n, x, y, w, work);
+  sum_partials_kernel<<<1, kT, 0, s>>>(nb, work, out);
+  return cuda_status(cudaGetLastError());
+}
+
 extern "C" int ddmgnn_axpy2(int64_t n, double alpha, const double* p, const double* q,
                             double* u, double* r, double* work, double* rr_out, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -172,13 +193,13 @@ extern "C" int ddmgnn_prolong(int64_t n, int two_level, const int32_t* tptr,
 
 // ---------------------------------------------------------------- device-side scalars
 // Distributed PCG with its scalars on the device (no host round trip per dot):
-// st[] = {rho, pq, alpha, rr, nb, tol, rz, beta, iter, status, max_iter}; the
+// st[] = {rho, pq, alpha, rr, nb, tol, rz, beta, iter, status, max_iter, rzo}; the
 // all-reduces of pq, rr, rz operate on st[1], st[3], st[6] in place, and the
 // updates below become no-ops once status != 0 (converged / not SPD / non-finite),
 // so the host only polls the status every few iterations.
 namespace ddmgnn {
 namespace {
-enum { kRho, kPq, kAlpha, kRr, kNb, kTol, kRz, kBeta, kIter, kStatus, kMaxIter };
+enum { kRho, kPq, kAlpha, kRr, kNb, kTol, kRz, kBeta, kIter, kStatus, kMaxIter, kRzo };
 
 __global__ void pcg_scalars_kernel(int op, double* st, double* hist) {
   if (st[kStatus] != 0.0) return;
@@ -196,8 +217,11 @@ __global__ void pcg_scalars_kernel(int op, double* st, double* hist) {
     hist[it] = rel;
     if (rel < st[kTol]) st[kStatus] = 1.0;
     else if (it >= static_cast<int>(st[kMaxIter])) st[kStatus] = 2.0;
-  } else {  // beta = rho' / rho, rho = rho' (sparse.py:123-125)
+  } else if (op == 2) {  // beta = rho' / rho, rho = rho' (sparse.py:123-125)
     st[kBeta] = st[kRz] / st[kRho];
+    st[kRho] = st[kRz];
+  } else {  // flexible CG: beta = <r, z - z_old> / rho, rho = rho'
+    st[kBeta] = st[kRzo] / st[kRho];
     st[kRho] = st[kRz];
   }
 }
@@ -233,7 +257,7 @@ __global__ void xpby_dev_kernel(long long n, const double* __restrict__ z,
 }  // namespace ddmgnn
 
 extern "C" int ddmgnn_pcg_scalars(int op, double* st, double* hist, void* stream) {
-  if (op < 0 || op > 2) return kValueError;
+  if (op < 0 || op > 3) return kValueError;
   pcg_scalars_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(op, st, hist);
   return cuda_status(cudaGetLastError());
 }

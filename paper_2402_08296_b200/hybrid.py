@@ -24,6 +24,7 @@ from . import _lib
 from .asm import coarse_inverse, coarse_matrix
 from .decomp import Decomposition
 from .dss import DssModel, flat_params
+from .sparse import private_copy
 
 __all__ = ["DdmGnnPreconditioner", "build_ddm_gnn", "apply_ddm_gnn", "plan_batches",
            "LocalGraphView"]
@@ -133,7 +134,8 @@ def build_ddm_gnn(a: sp.csr_matrix, coords: np.ndarray, dec: Decomposition, mode
             raise RuntimeError(msg if msg.startswith("singular coarse matrix")
                                else f"singular coarse matrix: {msg}") from exc
         ctx.set_coarse_inverse(inv)
-    return DdmGnnPreconditioner(ctx, a, dec, model, level, batch_nodes_cap, cm)
+    # private copy: pcg() recognises "its" matrix by content, not identity
+    return DdmGnnPreconditioner(ctx, private_copy(a), dec, model, level, batch_nodes_cap, cm)
 
 
 def _is_torch_cuda(x) -> bool:

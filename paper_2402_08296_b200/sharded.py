@@ -523,9 +523,11 @@ class ShardedDdmGnn:
         return full
 
     # -- Krylov -----------------------------------------------------------------------------
-    def pcg(self, b_global, tol: float, max_iter: int, check_every: int = 8):
+    def pcg(self, b_global, tol: float, max_iter: int, check_every: int = 8,
+            flexible: bool = False):
         """Distributed PCG (sparse.py:76-127) with this preconditioner; collective.
-        Returns (u_global, SolveReport) on every rank.
+        Returns (u_global, SolveReport) on every rank.  ``flexible=True``: the opt-in
+        flexible CG (beta = <r, z - z_old> / rho), as ``sparse.pcg``.
 
         The recurrence's scalars live on the device (``st``, see ddmgnn_pcg_scalars):
         <p, Ap>, ||r||^2 and <r, z> are reduced into it in place by the all-reduces,
@@ -545,15 +547,21 @@ class ShardedDdmGnn:
         u = torch.zeros_like(bo)
         r = bo.clone()
         q = torch.empty_like(bo)
-        st = torch.zeros(11, dtype=torch.float64, device=self.device)
+        max_iter = max(0, int(max_iter))  # sparse.py:105: no iteration for max_iter < 0
+        st = torch.zeros(12, dtype=torch.float64, device=self.device)
         hist = torch.zeros(max_iter + 1, dtype=torch.float64, device=self.device)
         stream = self._stream
         self._dot(bo, bo, 0)
         nb = float(np.sqrt(self._allreduce_scalar(0)))
         if nb == 0.0:  # sparse.py:93-94
             return np.zeros(self.n), SolveReport(0, [0.0], True, 0.0, tol)
+        # r0 = b, so history[0] = ||b|| / ||b|| = 1 exactly (sparse.py:96-99)
+        if 1.0 < tol:
+            return np.zeros(self.n), SolveReport(0, [1.0], True, 1.0, tol)
         z = self.apply_owned(r)
+        self.ctx.apply_status(self._stream())  # non-finite model output -> reference error
         pv = z.clone()
+        z_old = torch.empty_like(z) if flexible else None
         self._c(lib.ddmgnn_dot(n_own, r.data_ptr(), z.data_ptr(), self.work.data_ptr(),
                                st[0:].data_ptr(), stream()))
         self.comm.allreduce_(st[0:1])  # rho = <r0, z0>
@@ -577,15 +585,24 @@ class ShardedDdmGnn:
             self.comm.allreduce_(st[3:4])
             self._c(lib.ddmgnn_pcg_scalars(1, st.data_ptr(), hist.data_ptr(), stream()))
             if (it + 1) % check_every == 0 or it + 1 == max_iter:
+                # the GNN status word of the applies since the last check, then the
+                # solve's own status (both are device-side words: one poll each)
+                self.ctx.apply_status(stream())
                 status = float(st[9].item())
                 if status != 0.0:
                     break
+            if flexible:
+                z_old.copy_(z)
             self.apply_owned(r, z)
             self._c(lib.ddmgnn_dot(n_own, r.data_ptr(), z.data_ptr(), self.work.data_ptr(),
                                    st[6:].data_ptr(), stream()))
+            if flexible:
+                self._c(lib.ddmgnn_dot_diff(n_own, r.data_ptr(), z.data_ptr(), z_old.data_ptr(),
+                                            self.work.data_ptr(), st[11:].data_ptr(), stream()))
+                self.comm.allreduce_(st[11:12])
             self.comm.allreduce_(st[6:7])
             s = stream()
-            self._c(lib.ddmgnn_pcg_scalars(2, st.data_ptr(), hist.data_ptr(), s))
+            self._c(lib.ddmgnn_pcg_scalars(3 if flexible else 2, st.data_ptr(), hist.data_ptr(), s))
             self._c(lib.ddmgnn_xpby_dev(n_own, z.data_ptr(), st.data_ptr(), pv.data_ptr(), s))
         sh = st.cpu().numpy()
         status, iters = int(sh[9]), int(sh[8])

@@ -5,7 +5,9 @@
     SolveReport                                                      sparse.py:31-53
 
 The recurrence is the reference's Algorithm 1 exactly (standard PCG,
-beta = rho_{k+1}/rho_k), run on the GPU in fp64: CSR SpMV fused with <p,Ap>,
+beta = rho_{k+1}/rho_k; ``flexible=True`` opts into flexible CG, Polak-Ribiere
+beta = <r_{k+1}, z_{k+1} - z_k>/rho_k, which the reference does not have), run
+on the GPU in fp64: CSR SpMV fused with <p,Ap>,
 fused axpy + norm, the preconditioner kernels, all captured in a CUDA graph.
 ``precond`` may be
   * a DdmGnnPreconditioner built on the same matrix -> fully on device;
@@ -24,7 +26,7 @@ import scipy.sparse as sp
 
 from . import _lib
 
-__all__ = ["SolveReport", "validate_csr", "pcg", "cg", "Ic0Preconditioner", "ic0"]
+__all__ = ["SolveReport", "validate_csr", "pcg", "fcg", "cg", "Ic0Preconditioner", "ic0"]
 
 
 @dataclass
@@ -54,18 +56,28 @@ def validate_csr(a: sp.csr_matrix) -> None:
     d = np.diff(indices)
     row_of = np.repeat(np.arange(n_rows), np.diff(indptr))
     same_row = row_of[1:] == row_of[:-1]
-    bad = same_row & (d <= 0)
-    if np.any(bad) or (indices.size and (indices.min() < 0 or indices.max() >= n_cols)):
-        r = int(row_of[1:][bad][0]) if np.any(bad) else 0
+    # the reference scans rows in order and reports the first row that breaks
+    # either rule (sparse.py:64-67)
+    bad_rows = np.zeros(n_rows, dtype=bool)
+    bad_rows[row_of[1:][same_row & (d <= 0)]] = True
+    bad_rows[row_of[(indices < 0) | (indices >= n_cols)]] = True
+    if np.any(bad_rows):
+        r = int(np.argmax(bad_rows))
         raise ValueError(f"row {r}: columns not strictly increasing in range")
 
 
 _solver_cache: dict = {}
 
 
+def private_copy(a: sp.csr_matrix) -> sp.csr_matrix:
+    """A CSR copy that shares no array with the caller's matrix: device contexts
+    remember the matrix they hold through it, so an in-place edit of the caller's
+    ``a.data`` is seen as a different matrix (the reference recomputes ``a @ p``
+    on every call, sparse.py:107)."""
+    return sp.csr_matrix((a.data.copy(), a.indices.copy(), a.indptr.copy()), shape=a.shape)
+
+
 def _same_matrix(a, b) -> bool:
-    if a is b:
-        return True
     return (a.shape == b.shape and a.nnz == b.nnz and np.array_equal(a.indptr, b.indptr)
             and np.array_equal(a.indices, b.indices) and np.array_equal(a.data, b.data))
 
@@ -77,7 +89,7 @@ def _solver_ctx(a, device: int = 0) -> _lib.Context:
         return hit[1]
     ctx = _lib.Context(device)
     ctx.set_matrix(a)
-    _solver_cache[device] = (a, ctx)
+    _solver_cache[device] = (private_copy(a), ctx)
     return ctx
 
 
@@ -89,8 +101,12 @@ def _as_csr(a):
     return a
 
 
-def pcg(a, b, precond, tol: float, max_iter: int, u0=None):
-    """Preconditioned conjugate gradient on the GPU; returns (u, SolveReport)."""
+def pcg(a, b, precond, tol: float, max_iter: int, u0=None, flexible: bool = False):
+    """Preconditioned conjugate gradient on the GPU; returns (u, SolveReport).
+
+    ``flexible=True``: flexible CG (beta = <r', z' - z>/rho) for nonlinear
+    preconditioners such as the GNN operator; an addition to the reference API
+    (its default, False, is the reference's recurrence, sparse.py:122-126)."""
     from .hybrid import DdmGnnPreconditioner
 
     if tol <= 0:
@@ -102,18 +118,27 @@ def pcg(a, b, precond, tol: float, max_iter: int, u0=None):
         if u0.shape != (n,):
             raise ValueError("u0 dimension mismatch")
     a = _as_csr(a)
+    if a.shape != (n, n):  # the reference fails in `b - a @ u` (sparse.py:96)
+        raise ValueError("dimension mismatch")
     from .asm import AsmPreconditioner
 
     if isinstance(precond, (DdmGnnPreconditioner, AsmPreconditioner, Ic0Preconditioner)) and \
             _same_matrix(precond.a, a):
         ctx, level = precond.context, precond._level_code
-        u, it, hist, conv = ctx.pcg(b, u0, tol, max_iter, level)
+        u, it, hist, conv = ctx.pcg(b, u0, tol, max_iter, level, flexible=flexible)
     elif precond is None:
-        u, it, hist, conv = _solver_ctx(a).pcg(b, u0, tol, max_iter, _lib.PRECOND_NONE)
+        u, it, hist, conv = _solver_ctx(a).pcg(b, u0, tol, max_iter, _lib.PRECOND_NONE,
+                                               flexible=flexible)
     else:
         fn = precond if callable(precond) else precond.__call__
-        u, it, hist, conv = _solver_ctx(a).pcg_host_precond(b, u0, tol, max_iter, fn)
+        u, it, hist, conv = _solver_ctx(a).pcg_host_precond(b, u0, tol, max_iter, fn,
+                                                            flexible=flexible)
     return u, SolveReport(it, hist, conv, hist[-1], tol)
+
+
+def fcg(a, b, precond, tol: float, max_iter: int, u0=None):
+    """Flexible CG (opt-in; ``pcg(..., flexible=True)``)."""
+    return pcg(a, b, precond, tol, max_iter, u0=u0, flexible=True)
 
 
 def cg(a, b, tol: float, max_iter: int, u0=None):
@@ -143,6 +168,9 @@ class Ic0Preconditioner:
 
     def __call__(self, x):
         x = np.asarray(x, dtype=float)
+        n = self.a.shape[0]
+        if x.shape != (n,):  # the reference's spsolve_triangular raises (sparse.py:177-179)
+            raise ValueError(f"expected vector of length {n}, got shape {x.shape}")
         return self._ctx.apply_host(x, self._level_code)
 
 
@@ -157,5 +185,5 @@ def ic0(a: sp.csr_matrix, device: int = 0) -> Ic0Preconditioner:
     ctx = _lib.Context(device)
     ctx.set_matrix(a)
     ctx.set_ic0()
-    return Ic0Preconditioner(ctx, a)
+    return Ic0Preconditioner(ctx, private_copy(a))
 

@@ -149,3 +149,22 @@ def test_gnn_launch_count():
     assert count(K=50, n_big=50, n_cluster=50, cluster_launches=2) == 2  # clusters only
     assert count(n_big=3, n_cluster=0) == 1 + 1 + 20                     # flat path
     assert count(k_bar=30, n_chunks=3, n_big=2, n_cluster=1, cluster_launches=1) == 3 * 2 + 1 + 60
+
+
+def test_validate_csr_reports_first_bad_row():
+    """The reference scans rows in order (sparse.py:64-67): an out-of-range column
+    in row 4 is reported as row 4, before a later unsorted row."""
+    import scipy.sparse as sp
+
+    from paper_2402_08296_b200 import validate_csr
+
+    a = sp.csr_matrix(np.eye(8))
+    bad = sp.csr_matrix((a.data.copy(), a.indices.copy(), a.indptr.copy()), shape=(8, 8))
+    bad.indices[4] = 9
+    with pytest.raises(ValueError, match="row 4:"):
+        validate_csr(bad)
+    m = sp.csr_matrix(np.ones((6, 6)))
+    m.indices[m.indptr[5]:m.indptr[6]] = m.indices[m.indptr[5]:m.indptr[6]][::-1].copy()
+    m.indices[m.indptr[2] + 1] = -1
+    with pytest.raises(ValueError, match="row 2:"):
+        validate_csr(m)

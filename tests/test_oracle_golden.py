@@ -4,6 +4,8 @@ The fixtures come from tests/golden/make_golden.py (which imports
 /root/reference); the oracle restatement must reproduce them to fp64
 round-off, which makes it a trustworthy checker for the CUDA path.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -89,3 +91,36 @@ def test_desk_pcg_matches_reference():
     ref = g["desk_pcg_hist"]
     assert abs(it - (len(ref) - 1)) <= 1
     assert np.allclose(hist[:20], ref[:20], rtol=1e-8)
+
+
+def test_parallel_oracle_equals_serial_oracle():
+    """oracle/parallel.py (the multi-process oracle used at configs B/C/D and by
+    the bench's CPU legs) gives the serial oracle's z: same forward per subdomain,
+    same gluing order (hybrid.py:133-135)."""
+    from oracle.parallel import ParallelOracle
+
+    g = load_golden("A.npz")
+    a, _b, coords, subs = problem_from(g)
+    m = orc.model_from_flat(10, 10, float(g["m1010_alpha"]), 1, g["m1010_flat"])
+    ser = orc.OraclePreconditioner(a, coords, subs, m, "two")
+    with ParallelOracle(a, coords, subs, m, level="two", workers=3) as par:
+        assert par.workers == 3
+        for r in (g["r"], 2.0 * g["r"]):
+            assert rel_l2(par(r), ser(r)) < 1e-15
+            assert rel_l2(par.apply(r, "one"), g["m1010_z_loc"] * (1 if r is g["r"] else 2)) < 1e-12
+        desk = orc.load_model(os.path.join(os.path.dirname(__file__), "golden", "desk_k10_d10.dss"))
+        par.set_model(desk)
+        assert rel_l2(par(g["r"]), g["desk_z_two"]) < 1e-13
+
+
+def test_oracle_flexible_cg():
+    """Flexible CG (opt-in; Polak-Ribiere beta): with z = r it is CG in exact
+    arithmetic (r_k+1 . r_k = 0), so it needs the reference CG's iteration count
+    to +-1; its default (flexible=False) is the reference recurrence."""
+    g = load_golden("small.npz")
+    a, b, _c, _s = problem_from(g)
+    _u, it, hist, conv = orc.pcg(a, b, None, 1e-8, 500, flexible=True)
+    assert conv and abs(it - int(g["cg_iters"])) <= 1
+    _u, it0, hist0, _ = orc.pcg(a, b, None, 1e-8, 500)
+    assert np.allclose(hist0, g["cg_hist"], rtol=1e-10)
+    assert np.allclose(hist[:10], hist0[:10], rtol=1e-9)
