@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--d", type=int, default=10)
     ap.add_argument("--level", default="two", choices=["one", "two"])
     ap.add_argument("--weights", default="random", help="'random' or a dss-v1 file")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-pcg", action="store_true")
     ap.add_argument("--pcg-weights", default=os.path.join(ROOT, "tests", "golden", "desk_k10_d10.dss"),
                     help="weights of the time-to-solution leg (trained; random weights do not "
@@ -152,12 +152,33 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
-def build_workload(args):
-    from paper_2402_08296_b200.problem import ProblemConfig, build_problem
+def load_workload(args, build_in_child):
+    """The cached config (workload.py): both arms time the same A, b, coords and
+    subdomains; the reference process reads it with numpy only."""
+    import workload
 
-    t0 = time.perf_counter()
-    prob = build_problem(0, ProblemConfig(args.target_nodes, 0.2, args.subdomain_size, args.overlap))
-    return prob, time.perf_counter() - t0
+    return workload.load(args.target_nodes, args.subdomain_size, args.overlap,
+                         build_in_child=build_in_child)
+
+
+def weights_desc(args):
+    return ("random init_model(%d,%d,seed=1)" % (args.kbar, args.d) if args.weights == "random"
+            else os.path.relpath(args.weights, ROOT))
+
+
+def config_obj(args, w, world):
+    """The `config` object both arms print (identical for the same launch)."""
+    return {
+        "workload": f"C: blob mesh target {args.target_nodes} nodes (N={w.n}), "
+                    f"N_s={args.subdomain_size}, overlap {args.overlap}, K={w.k}, V={w.v}, "
+                    f"{args.level}-level DDM-GNN k_bar={args.kbar} d={args.d}, weights "
+                    f"{weights_desc(args)}",
+        "step": "one full preconditioner apply z = M r (hybrid.py:112-136: restriction, "
+                "K local GNN solves, coarse solve, gluing) on r = default_rng(0).standard_normal(N)",
+        "l2": "GPU arm: L2 flushed (256 MB write) before every timed step",
+        "parallelism": f"{world} GPU rank(s)" + (" (subdomain shards)" if world > 1 else "")
+                       + "; reference arm: rank 0 on all host cores",
+    }
 
 
 def load_model(args):
@@ -168,77 +189,192 @@ def load_model(args):
     return ddm.load_model(args.weights)
 
 
-# ----------------------------------------------------------------------------- CPU baseline
-
-
-def cpu_baseline(prob, args, seconds):
-    """Oracle restatement of the reference apply (numpy/OpenBLAS, all host threads)
-    on a bounded sample of subdomains, extrapolated linearly in subdomain nodes."""
+def oracle_model(args):
     from oracle import ddm_oracle as orc
 
-    import paper_2402_08296_b200 as ddm
+    if args.weights == "random":
+        return orc.model_from_flat(args.kbar, args.d, 1e-3, 1,
+                                   orc.init_model_flat(args.kbar, args.d, 1))
+    return orc.load_model(args.weights)
 
-    model = load_model(args)
-    om = orc.model_from_flat(model.k_bar, model.d, model.alpha, model.seed, ddm.flat_params(model))
-    subs = prob.dec.subdomains
-    a = prob.system.a
-    rng = np.random.default_rng(0)
-    r = rng.standard_normal(a.shape[0])
-    v_total = sum(s.size for s in subs)
-    sample, v_s = [], 0
-    # sample sized so one forward is ~1/3 of the budget at ~30 us/node
-    target_nodes = max(2000, int(seconds / 3 / 3e-5))
-    for i in range(len(subs)):
-        sample.append(i)
-        v_s += subs[i].size
-        if v_s >= target_nodes:
-            break
-    graphs = [orc.local_graph(a, subs[i], prob.coords) for i in sample]
-    cs = []
-    for i in sample:
-        ri = r[subs[i]]
-        cs.append(ri / np.linalg.norm(ri))
-    reps, t0 = 0, time.perf_counter()
-    while True:
+
+# ----------------------------------------------------------------------------- CPU legs
+
+
+def host_info():
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(),
+            "blas_threads_per_process": 1,
+            "numpy": np.__version__}
+
+
+def cpu_full_applies(w, args, steps, warmup, workers=None):
+    """The reference's full apply (hybrid.py:112-136 restated in oracle/ddm_oracle.py
+    and spread over host cores by oracle/parallel.py: all K subdomains' forwards,
+    the coarse lu_solve and the gluing) timed per step on the host clock."""
+    from oracle.parallel import ParallelOracle
+
+    r = np.random.default_rng(0).standard_normal(w.n)
+    t0 = time.perf_counter()
+    with ParallelOracle(w.a, w.coords, w.subdomains, oracle_model(args), level=args.level,
+                        workers=workers) as par:
+        t_setup = time.perf_counter() - t0
+        for _ in range(warmup):
+            par(r)
+        times = []
+        for _ in range(steps):
+            t1 = time.perf_counter()
+            z = par(r)
+            times.append(time.perf_counter() - t1)
+        # where the time goes on the host: the parent's coarse solve + gluing
+        t1 = time.perf_counter()
+        if args.level == "two":
+            par.coarse_term(r)
+        t_coarse = time.perf_counter() - t1
+        nw = par.workers
+    return {"times_s": times, "setup_s": t_setup, "workers": nw, "coarse_s": t_coarse,
+            "z_norm": float(np.linalg.norm(z))}
+
+
+def cpu_single_core(w, args, frac=0.03, seed=0):
+    """One core (one process, one BLAS thread): the oracle forward over a random
+    sample of subdomains, extrapolated linearly in subdomain nodes."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import ddm_oracle as orc
+
+    rng = np.random.default_rng(seed)
+    k = w.k
+    sample = np.sort(rng.choice(k, max(1, int(round(frac * k))), replace=False))
+    om = oracle_model(args)
+    r = np.random.default_rng(0).standard_normal(w.n)
+    graphs = [orc.local_graph(w.a, w.subdomains[i], w.coords) for i in sample]
+    cs = [r[w.subdomains[i]] / np.linalg.norm(r[w.subdomains[i]]) for i in sample]
+    v_s = sum(g.node_count for g in graphs)
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
         orc.forward(om, graphs, cs)
-        reps += 1
-        el = time.perf_counter() - t0
-        if el >= seconds / 3 or reps >= 3:
-            break
-    per_apply_s = el / reps * (v_total / v_s)
+        t = time.perf_counter() - t0
+    return {"seconds_per_apply_extrapolated": t * w.v / v_s,
+            "sample": f"{sample.size}/{k} random subdomains ({v_s}/{w.v} subdomain nodes), "
+                      f"forward only, 1 process x 1 BLAS thread, extrapolated linearly in V"}
+
+
+def cpu_pcg_config_a():
+    """The reference's end-to-end PCG-DDM-GNN (sparse.py:76-127 + hybrid.py:112-136,
+    restated) at BASELINE config A with the pinned desk weights, one worker
+    process per subdomain (oracle/parallel.py)."""
+    import scipy.sparse as sp
+
+    from oracle import ddm_oracle as orc
+
+    g = np.load(os.path.join(ROOT, "tests", "golden", "A.npz"))
+    n = g["b"].shape[0]
+    a = sp.csr_matrix((g["data"], g["indices"], g["indptr"]), shape=(n, n))
+    ptr, idx = g["sub_ptr"], g["sub_idx"]
+    subs = [idx[ptr[i]:ptr[i + 1]] for i in range(len(ptr) - 1)]
+    from oracle.parallel import ParallelOracle
+
+    m = orc.load_model(os.path.join(ROOT, "tests", "golden", "desk_k10_d10.dss"))
+    t0 = time.perf_counter()
+    with ParallelOracle(a, g["coords"], subs, m, level="two") as pre:
+        t_setup = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        _u, it, hist, conv = orc.pcg(a, g["b"], pre, 1e-6, 500)
+        secs = time.perf_counter() - t0
+        nw = pre.workers
+    return {"config": "A (N=%d, K=%d)" % (n, len(subs)), "seconds": secs,
+            "iterations": it, "converged": conv, "final_relres": hist[-1],
+            "setup_s": t_setup, "weights": "tests/golden/desk_k10_d10.dss",
+            "processes": nw, "blas_threads_per_process": 1}
+
+
+def cpu_pcg_record(cfg):
+    """Recorded CPU PCG of a config too long for every bench run (tools/cpu_pcg.py)."""
+    import glob
+
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_cpu_pcg_{cfg}.json")),
+                       reverse=True):
+        try:
+            rec = json.load(open(path))
+            rec["record"] = os.path.relpath(path, ROOT)
+            return rec
+        except (OSError, ValueError):
+            continue
+    return None
+
+
+def cpu_baseline(w, args, steps=2):
+    """cpu_baseline of the GPU arm (rank 0, N=1): full oracle applies on all host
+    cores (a bounded sample of the workload: `steps` applies), the one-core figure,
+    and the CPU time-to-solution at config A (and B from its record)."""
+    full = cpu_full_applies(w, args, steps=steps, warmup=1)
+    sec = float(np.median(full["times_s"]))
+    single = cpu_single_core(w, args)
     return {
-        "value": 1.0 / per_apply_s,
-        "unit": UNIT,
-        "cores": os.cpu_count(),
-        "kind": "port",
-        "sample": f"{len(sample)}/{len(subs)} subdomains ({v_s}/{v_total} subdomain nodes), "
-                  f"{reps} forward(s) of oracle/ddm_oracle.py (restatement of dss.py:302-329), "
-                  f"extrapolated linearly in subdomain nodes; restriction/coarse/gluing (<2% on the "
-                  f"reference) not included",
-        "seconds_per_apply": per_apply_s,
+        "value": 1.0 / sec, "unit": UNIT, "cores": full["workers"], "kind": "port",
+        "sample": f"{steps} full applies (all {w.k} subdomains + coarse lu_solve + gluing, "
+                  f"hybrid.py:112-136) of oracle/ddm_oracle.py over {full['workers']} "
+                  f"processes x 1 BLAS thread (oracle/parallel.py), after 1 warm-up apply",
+        "seconds_per_apply": sec, "seconds_per_apply_all": full["times_s"],
+        "coarse_solve_s": full["coarse_s"], "setup_s": full["setup_s"],
+        "single_core": single, "host": host_info(),
+        "pcg_config_a": cpu_pcg_config_a(), "pcg_config_b": cpu_pcg_record("B"),
     }
 
 
+def mapped_repo_libs():
+    """Shared objects of this repository mapped into this process (/proc/self/maps)."""
+    found = set()
+    try:
+        for line in open("/proc/self/maps"):
+            path = line.split()[-1] if line.strip() else ""
+            if path.startswith(ROOT) and ".so" in os.path.basename(path):
+                found.add(os.path.relpath(path, ROOT))
+    except OSError:
+        pass
+    return sorted(found)
+
+
 def run_reference(args):
+    """--impl reference: the reference's CPU implementation of the path (the oracle
+    port of hybrid.py:112-136, pinned to the reference's own outputs) on all host
+    cores, one FULL apply of the config per step.  Rank 0 only; reads the workload
+    from the .npz cache (no native library of this repository in this process)."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    prob, _ = build_workload(args)
-    vals = []
-    for _ in range(args.warmup + args.steps if args.steps <= 2 else args.steps):
-        res = cpu_baseline(prob, args, max(3.0, args.cpu_seconds / max(1, args.steps)))
-        vals.append(res["value"])
-    v = float(np.median(vals))
-    res["value"] = v
+    w = load_workload(args, build_in_child=True)
+    res = cpu_full_applies(w, args, steps=args.steps, warmup=args.warmup)
+    times = res["times_s"]
+    ms = 1e3 * float(np.mean(times))
+    v = 1e3 / ms
     out = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / v,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": f"C: blob mesh {args.target_nodes} nodes, N_s={args.subdomain_size}, "
-                               f"overlap {args.overlap}, {args.level}-level DDM-GNN k_bar={args.kbar} d={args.d}"},
-        "cpu_baseline": res,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak" if world == 1 else "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_obj(args, w, world),
+        "cpu_baseline": {
+            "value": v, "unit": UNIT, "cores": res["workers"], "kind": "port",
+            "sample": f"every step one full apply over all {w.k} subdomains (forwards + coarse "
+                      f"lu_solve + gluing, hybrid.py:112-136), oracle/ddm_oracle.py over "
+                      f"{res['workers']} processes x 1 BLAS thread (oracle/parallel.py)",
+            "seconds_per_step": times, "setup_s": res["setup_s"], "host": host_info(),
+        },
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "problem_source": w.source,
+        "native_libs_mapped": mapped_repo_libs(),
+        "pcg_config_a": cpu_pcg_config_a(),
+        "pcg_config_b": cpu_pcg_record("B"),
     }
     print(json.dumps(out))
 
@@ -246,37 +382,65 @@ def run_reference(args):
 # ----------------------------------------------------------------------------- GPU arm
 
 
-def time_to_solution(ddm, p, prob, args, ctx, lvl, dev, stream, weights=None):
-    """Device-timed PCG (sparse.py:76-127) to 1e-6 with the pinned trained weights:
-    warm-up solve (captures the CUDA graphs), then one solve between CUDA events
-    on the solve's stream; setup excluded (as cli.py:195-199 minus the build)."""
+def time_to_solution(ddm, p, a, b_host, args, lvl, dev, stream, weights=None, flexible=False,
+                     restore=True):
+    """Device-timed PCG (sparse.py:76-127) to 1e-6 with trained weights: warm-up
+    solve (captures the CUDA graphs), then one solve between CUDA events on the
+    solve's stream; setup excluded (as cli.py:195-199 minus the build).
+    ``flexible``: the opt-in flexible CG."""
     import torch
 
+    ctx = p.context
     weights = weights or args.pcg_weights
-    model = ddm.load_model(weights)
-    p.reload_model(model)
-    b = torch.tensor(prob.system.b, device=dev)
+    p.reload_model(ddm.load_model(weights))
+    b = torch.tensor(b_host, device=dev)
     u = torch.empty_like(b)
     s = stream.cuda_stream
-    _u, it0, _h, conv0 = ctx.pcg(b.data_ptr(), None, 1e-6, args.pcg_max_iter, lvl, True,
-                                 u.data_ptr(), s)
+    ctx.pcg(b.data_ptr(), None, 1e-6, args.pcg_max_iter, lvl, True, u.data_ptr(), s,
+            flexible=flexible)
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     _u, it, hist, conv = ctx.pcg(b.data_ptr(), None, 1e-6, args.pcg_max_iter, lvl, True,
-                                 u.data_ptr(), s)
+                                 u.data_ptr(), s, flexible=flexible)
     e1.record(stream)
     torch.cuda.synchronize(dev)
     sec = e0.elapsed_time(e1) / 1e3
     uh = u.cpu().numpy()
-    a = prob.system.a
-    true_rel = float(np.linalg.norm(prob.system.b - a @ uh) / np.linalg.norm(prob.system.b))
-    p.reload_model(load_model(args))
+    true_rel = float(np.linalg.norm(b_host - a @ uh) / np.linalg.norm(b_host))
+    if restore:
+        p.reload_model(load_model(args))
     return {"seconds": sec, "iterations": it, "converged": conv, "final_relres": hist[-1],
             "true_relres": true_rel, "ms_per_iteration": 1e3 * sec / max(1, it),
-            "max_iter": args.pcg_max_iter, "tol": 1e-6,
+            "max_iter": args.pcg_max_iter, "tol": 1e-6, "solver": "fcg" if flexible else "pcg",
             "weights": os.path.relpath(weights, ROOT),
             "timing": "CUDA events on the solve stream, device-resident b/u, graphs warm"}
+
+
+def gpu_tts_small(ddm, args, dev, stream):
+    """Device time-to-solution at BASELINE configs A and B (desk weights, two-level),
+    beside the CPU's (cpu_baseline.pcg_config_a / pcg_config_b)."""
+    import scipy.sparse as sp
+
+    from paper_2402_08296_b200.problem import ProblemConfig, build_problem
+
+    out = {}
+    g = np.load(os.path.join(ROOT, "tests", "golden", "A.npz"))
+    n = g["b"].shape[0]
+    a = sp.csr_matrix((g["data"], g["indices"], g["indptr"]), shape=(n, n))
+    ptr, idx = g["sub_ptr"], g["sub_idx"]
+    subs = [idx[ptr[i]:ptr[i + 1]] for i in range(len(ptr) - 1)]
+    dec = ddm.finish_decomposition(subs, g["owner"], int(g["overlap"]))
+    problems = {"A": (a, g["b"], g["coords"], dec)}
+    pb = build_problem(0, ProblemConfig(100_000, 0.2, 1000, 2))
+    problems["B"] = (pb.system.a, pb.system.b, pb.coords, pb.dec)
+    for name, (a, b, coords, dec) in problems.items():
+        model = ddm.load_model(args.pcg_weights)
+        p = ddm.build_ddm_gnn(a, coords, dec, model, level="two", device=dev.index or 0)
+        out[name] = time_to_solution(ddm, p, a, b, args, 2, dev, stream, restore=False)
+        out[name]["config"] = f"{name} (N={b.size}, K={dec.n_subdomains})"
+        del p
+    return out
 
 
 def run_ours(args):
@@ -297,22 +461,25 @@ def run_ours(args):
         else:
             dist.init_process_group(backend)
         return run_sharded(args, world, rank, local)
+    w = load_workload(args, build_in_child=False)
+    # the CPU baseline first, before this process initialises CUDA (its worker
+    # processes are forked)
+    cpu = cpu_baseline(w, args) if (world == 1 and rank == 0 and not args.no_cpu) else None
     torch.cuda.set_device(local)
 
     import paper_2402_08296_b200 as ddm
 
-    prob, t_setup = build_workload(args)
+    dec = ddm.finish_decomposition(w.subdomains, w.owner, w.overlap)
     model = load_model(args)
     t0 = time.perf_counter()
-    p = ddm.build_ddm_gnn(prob.system.a, prob.coords, prob.dec, model, level=args.level,
-                          device=local)
+    p = ddm.build_ddm_gnn(w.a, w.coords, dec, model, level=args.level, device=local)
     t_build = time.perf_counter() - t0
     info = p.info()
     ctx = p.context
-    n = prob.system.n
+    n = w.n
     lvl = 2 if args.level == "two" else 1
     dev = torch.device(f"cuda:{local}")
-    r = torch.tensor(np.random.default_rng(rank).standard_normal(n), device=dev)
+    r = torch.tensor(np.random.default_rng(0).standard_normal(n), device=dev)
     z = torch.empty_like(r)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > L2
     stream = torch.cuda.Stream(dev)  # events and kernels on the same (non-default) stream
@@ -359,7 +526,7 @@ def run_ours(args):
     value = world * 1e3 / ms_max
 
     # ---- SpMV roofline (HBM) ----
-    a = prob.system.a
+    a = w.a
     x = torch.tensor(np.ones(n), device=dev)
     y = torch.empty_like(x)
     for _ in range(3):
@@ -375,7 +542,7 @@ def run_ours(args):
     spmv_bytes = 12 * a.nnz + 20 * n
 
     # ---- end to end through the C ABI with host buffers (pinned, per the contract) ----
-    r_pin = torch.from_numpy(np.random.default_rng(rank).standard_normal(n)).pin_memory()
+    r_pin = torch.from_numpy(np.random.default_rng(0).standard_normal(n)).pin_memory()
     z_pin = torch.empty(n, dtype=torch.float64).pin_memory()
     r_host, z_host = r_pin.numpy(), z_pin.numpy()
     # host-clocked, so more steps than the device-timed loop (short host-timed
@@ -396,15 +563,18 @@ def run_ours(args):
     e2e_value = world / float(e2e_t.item())
 
     # ---- time-to-solution: device-resident PCG to 1e-6 (trained weights) ----
-    pcg = pcg_trained = None
+    pcg = pcg_trained = pcg_flex = tts_small = None
     if not args.no_pcg:
-        pcg = time_to_solution(ddm, p, prob, args, ctx, lvl, dev, stream)
+        pcg = time_to_solution(ddm, p, w.a, w.b, args, lvl, dev, stream)
+        pcg_flex = time_to_solution(ddm, p, w.a, w.b, args, lvl, dev, stream, flexible=True)
         # weights trained on the GPU for this subdomain size (tools/train_gpu.py), if present
         for cand in ("gpu_k10_ns1000_long.dss", "gpu_k10_ns1000.dss"):
             path = os.path.join(ROOT, "weights", cand)
             if os.path.exists(path) and args.subdomain_size == 1000 and args.kbar == 10:
-                pcg_trained = time_to_solution(ddm, p, prob, args, ctx, lvl, dev, stream, path)
+                pcg_trained = time_to_solution(ddm, p, w.a, w.b, args, lvl, dev, stream, path)
                 break
+        if world == 1:
+            tts_small = gpu_tts_small(ddm, args, dev, stream)
 
     peaks = {}
     try:
@@ -427,26 +597,14 @@ def run_ours(args):
     per_step_launches = n_gnn_launches + (1 if lvl == 2 else 0) + 1
     clocks = clk.summary()
     if rank == 0:
-        cpu = cpu_baseline(prob, args, args.cpu_seconds) if world == 1 else None
-        if cpu is not None and pcg is not None:
-            # the reference PCG's cost is ~all in apply
-            cpu["time_to_solution_s_extrapolated"] = cpu["seconds_per_apply"] * (pcg["iterations"] + 1)
-            cpu["time_to_solution_note"] = ("per-apply CPU time x (GPU iteration count + 1); the "
-                                            "reference's SpMV/BLAS-1 (<1%) not included")
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32 GNN / f64 Krylov+gluing",
             "data": "synthetic (reference problem generator restated natively; random-init weights)",
-            "config": {
-                "workload": f"C: blob mesh target {args.target_nodes} nodes (N={n}), "
-                            f"N_s={args.subdomain_size}, overlap {args.overlap}, K={info['K']}, "
-                            f"V={info['V']}, E={info['E']}, {args.level}-level DDM-GNN "
-                            f"k_bar={info['k_bar']} d={info['d']}",
-                "step": "one preconditioner apply z = M r",
-                "l2": "flushed (256 MB write) before every timed step",
-                "parallelism": f"{world} rank(s); each rank owns a full config-C instance",
-            },
+            "config": config_obj(args, w, world),
+            "layout": {"E": info["E"], "E_pad": info["E_pad"], "k_max": info["k_max"],
+                       "n_cluster": info["n_cluster"], "problem_source": w.source},
             "roofline": {
                 "kernel": "gnn_kernel + concurrent gnn_cluster_kernel (fused restriction + "
                           f"{info['k_bar']} message-passing layers + decoder)",
@@ -473,8 +631,10 @@ def run_ours(args):
             "gpu_launches": per_step_launches * args.steps,
             "clocks": clocks,
             "pcg": pcg,
+            "pcg_flexible": pcg_flex,
             "pcg_trained_weights": pcg_trained,
-            "setup_s": {"problem_build": t_setup, "preconditioner_build": t_build},
+            "time_to_solution_small": tts_small,
+            "setup_s": {"problem_load": w.seconds, "preconditioner_build": t_build},
         }
         print(json.dumps(out))
     if world > 1:
@@ -493,13 +653,14 @@ def run_sharded(args, world, rank, local):
     from paper_2402_08296_b200.sharded import ShardedDdmGnn
 
     dev = torch.device(f"cuda:{local}")
-    prob, t_setup = build_workload(args)
+    w = load_workload(args, build_in_child=False)
+    dec = ddm.finish_decomposition(w.subdomains, w.owner, w.overlap)
     model = load_model(args)
     t0 = time.perf_counter()
-    sh = ShardedDdmGnn(prob.system.a, prob.coords, prob.dec, model, level=args.level, device=local,
+    sh = ShardedDdmGnn(w.a, w.coords, dec, model, level=args.level, device=local,
                        exchange=args.exchange)
     t_build = time.perf_counter() - t0
-    r_glob = np.random.default_rng(0).standard_normal(prob.system.n)
+    r_glob = np.random.default_rng(0).standard_normal(w.n)
     r = sh.owned_part(r_glob)
     z = torch.empty_like(r)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
@@ -535,11 +696,11 @@ def run_sharded(args, world, rank, local):
     dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
     pcg = None
     if not args.no_pcg:
-        sh2 = ShardedDdmGnn(prob.system.a, prob.coords, prob.dec, ddm.load_model(args.pcg_weights),
+        sh2 = ShardedDdmGnn(w.a, w.coords, dec, ddm.load_model(args.pcg_weights),
                             level=args.level, device=local, exchange=args.exchange)
         dist.barrier()
         t0 = time.perf_counter()
-        u, rep = sh2.pcg(prob.system.b, 1e-6, args.pcg_max_iter)
+        u, rep = sh2.pcg(w.b, 1e-6, args.pcg_max_iter)
         tt = torch.tensor([time.perf_counter() - t0], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         pcg = {"seconds": float(tt.item()), "iterations": rep.iterations,
@@ -552,18 +713,12 @@ def run_sharded(args, world, rank, local):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32 GNN / f64 Krylov+gluing",
             "data": "synthetic (reference problem generator restated natively; random-init weights)",
-            "config": {"workload": f"blob mesh target {args.target_nodes} nodes (N={prob.system.n}), "
-                                   f"N_s={args.subdomain_size}, overlap {args.overlap}, "
-                                   f"K={prob.dec.n_subdomains}, {args.level}-level, sharded over "
-                                   f"{world} ranks (RCB groups of subdomains)",
-                       "step": "one preconditioner apply z = M r over the whole problem",
-                       "l2": "flushed (256 MB write) before every timed step",
-                       "parallelism": f"{world} ranks, subdomain shards + NCCL halo/term exchange"},
+            "config": config_obj(args, w, world),
             "e2e": {"value": 1.0 / float(e2e.item()), "unit": UNIT,
-                    "h2d_bytes_per_step": 8 * prob.system.n, "d2h_bytes_per_step": 8 * prob.system.n},
+                    "h2d_bytes_per_step": 8 * sh.plan.n_own, "d2h_bytes_per_step": 8 * sh.plan.n_own},
             "gpu_launches": sh.launches_per_apply() * args.steps, "clocks": clk.summary(),
             "pcg": pcg,
-            "setup_s": {"problem_build": t_setup, "preconditioner_build": t_build},
+            "setup_s": {"problem_load": w.seconds, "preconditioner_build": t_build},
         }
         print(json.dumps(out))
     dist.destroy_process_group()

@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 def test_bench_json_line_small():
     out = subprocess.run(
         [sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "3", "--warmup", "3",
-         "--target-nodes", "100000", "--cpu-seconds", "1"],
+         "--target-nodes", "100000"],
         capture_output=True, text=True, timeout=900, check=True)
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1
@@ -32,3 +32,5 @@ def test_bench_json_line_small():
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["pcg"]["converged"] and d["pcg"]["true_relres"] < 1.01e-6
     assert d["cpu_baseline"]["value"] > 0
+    assert d["pcg_flexible"]["converged"]
+    assert d["time_to_solution_small"]["A"]["converged"]

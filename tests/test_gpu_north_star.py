@@ -100,8 +100,10 @@ def test_config_c_apply_matches_oracle(ddm, config_c, oracle_c, weights):
         assert np.array_equal(zt.cpu().numpy(), z)
         del p
     if weights == "desk":
-        # trained weights: the GNN term dominates (SURVEY.md finding 5)
-        assert np.linalg.norm(z_loc_ref) > np.linalg.norm(z_two_ref - z_loc_ref)
+        # trained weights: the GNN term is a large share of z (0.56 of the coarse
+        # term's norm at C with the desk weights; 3e-3 with random weights,
+        # SURVEY.md finding 5), so the two-level bar exercises the GNN as well
+        assert np.linalg.norm(z_loc_ref) > 0.3 * np.linalg.norm(z_two_ref - z_loc_ref)
 
 
 # ------------------------------------------------------------------ PCG iteration parity
