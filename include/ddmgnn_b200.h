@@ -185,6 +185,47 @@ int ddmgnn_prolong(int64_t n, int two_level, const int32_t* tptr, const int32_t*
                    const double* pou, const double* y, const double* scale, const double* zloc,
                    double* z, void* stream);
 
+/* ---- Device-resident peer collectives (sharded solve without host barriers) ----
+ * g <= DDMGNN_PEER_MAX ranks, this rank `me`; flags[h] = rank h's flag block
+ * (int64[DDMGNN_PEER_FLAG_WORDS], zero-initialised, mapped into every rank with
+ * CUDA IPC); chan < DDMGNN_PEER_CHANNELS names one call site.  Ordering is by
+ * device-side epochs and acknowledgements, so the calls are stream-ordered and
+ * graph-capturable; every rank must make the same sequence of calls per channel.
+ * Host arrays: flags/dst/out/slots (g device pointers), send_off/recv_off (g + 1). */
+#define DDMGNN_PEER_MAX 8
+#define DDMGNN_PEER_CHANNELS 8
+#define DDMGNN_PEER_FLAG_WORDS (DDMGNN_PEER_CHANNELS * 32)
+/* Segment h of src[idx[send_off[h] .. send_off[h+1])] into dst[h] + dst_off[h]
+ * (rank h's receive buffer), then signal h. */
+int ddmgnn_peer_put(int g, int me, int chan, int64_t* const* flags, const double* src,
+                    const int32_t* idx, const int64_t* send_off, double* const* dst,
+                    const int64_t* dst_off, void* stream);
+/* Wait until every rank h with a non-empty receive segment [recv_off[h], recv_off[h+1])
+ * delivered this call's epoch; then ext[pos[i]] = recv[i] (pos may be NULL), and
+ * with ack != 0 acknowledge to the senders (else call ddmgnn_peer_ack after the
+ * kernel that consumes recv). */
+int ddmgnn_peer_wait(int g, int me, int chan, int64_t* const* flags, const int64_t* recv_off,
+                     const double* recv, const int32_t* pos, double* ext, int ack, void* stream);
+int ddmgnn_peer_ack(int g, int me, int chan, int64_t* const* flags, const int64_t* recv_off,
+                    void* stream);
+/* out[h] (rank h's [g][k] buffer) row me = in[0..k), on every rank. */
+int ddmgnn_peer_allgather(int g, int me, int chan, int64_t* const* flags, double* const* out,
+                          const double* in, int64_t k, void* stream);
+/* inout[0..k) = sum over ranks in rank order (k <= 16; identical bits on every
+ * rank); slots[h] = rank h's [g][k] staging area of this channel. */
+int ddmgnn_peer_allreduce(int g, int me, int chan, int64_t* const* flags, double* const* slots,
+                          double* inout, int k, void* stream);
+/* A wait that sees no peer for 30 s gives up and sets flags[me][DDMGNN_PEER_FLAG_WORDS - 1]
+ * (the host checks it when it polls the solve status). */
+/* Peer-visible buffers: zeroed cudaMalloc on `device`; 64-byte CUDA IPC handles;
+ * ddmgnn_ipc_open maps a peer's buffer into this process (lazy peer access from
+ * `device`, NVLink between the GPUs of one box). */
+int ddmgnn_peer_alloc(int device, int64_t bytes, void** ptr);
+int ddmgnn_peer_free(void* ptr);
+int ddmgnn_ipc_get(void* ptr, unsigned char* handle);
+int ddmgnn_ipc_open(int device, const unsigned char* handle, void** ptr);
+int ddmgnn_ipc_close(void* ptr);
+
 #ifdef __cplusplus
 }
 #endif

@@ -38,6 +38,7 @@ _pi64 = ctypes.POINTER(ctypes.c_int64)
 _pi32 = ctypes.POINTER(ctypes.c_int32)
 _pf = ctypes.POINTER(ctypes.c_float)
 _pint = ctypes.POINTER(ctypes.c_int)
+_pvp = ctypes.POINTER(ctypes.c_void_p)
 
 HOST_PRECOND_FN = ctypes.CFUNCTYPE(_int, _vp, _pd, _pd, _i64)
 
@@ -82,6 +83,16 @@ SIGNATURES = [
     ("ddmgnn_axpy2_dev", _int, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     ("ddmgnn_xpby_dev", _int, [_i64, _vp, _vp, _vp, _vp]),
     ("ddmgnn_prolong", _int, [_i64, _int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    ("ddmgnn_peer_put", _int, [_int, _int, _int, _pvp, _vp, _vp, _pi64, _pvp, _pi64, _vp]),
+    ("ddmgnn_peer_wait", _int, [_int, _int, _int, _pvp, _pi64, _vp, _vp, _vp, _int, _vp]),
+    ("ddmgnn_peer_ack", _int, [_int, _int, _int, _pvp, _pi64, _vp]),
+    ("ddmgnn_peer_allgather", _int, [_int, _int, _int, _pvp, _pvp, _vp, _i64, _vp]),
+    ("ddmgnn_peer_allreduce", _int, [_int, _int, _int, _pvp, _pvp, _vp, _int, _vp]),
+    ("ddmgnn_peer_alloc", _int, [_int, _i64, ctypes.POINTER(_vp)]),
+    ("ddmgnn_peer_free", _int, [_vp]),
+    ("ddmgnn_ipc_get", _int, [_vp, ctypes.c_char_p]),
+    ("ddmgnn_ipc_open", _int, [_int, ctypes.c_char_p, ctypes.POINTER(_vp)]),
+    ("ddmgnn_ipc_close", _int, [_vp]),
 ]
 
 _lib = None

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -103,6 +104,7 @@ struct ddmgnn_ctx {
   // coarse
   int coarse_k = 0;
   double* d_cinv = nullptr;
+  int coarse_ld = 0;         // leading dimension of d_cinv (K rounded up to even)
   // apply scratch
   double *d_r0r = nullptr, *d_scale = nullptr, *d_zloc = nullptr, *d_y = nullptr;
   float *d_hbuf = nullptr, *d_cbuf = nullptr, *d_qbuf = nullptr;
@@ -112,6 +114,9 @@ struct ddmgnn_ctx {
   int cluster_count[3] = {0, 0, 0};
   int cluster_smem[3] = {0, 0, 0}, cluster_threads[3] = {0, 0, 0};
   int two_cta = 1;            // CTA path: two CTAs per SM when they fit (DDMGNN_TWO_CTA)
+  int fused_tail = 0;         // PCG: one cooperative launch after the local solves (DDMGNN_FUSED_TAIL=1;
+                              // measured slower: 45 us vs 41 us for the three launches it replaces)
+  int h0_skip = 1;            // GNN layer 1 without its h rows (h = 0; DDMGNN_H0_SKIP)
   int *d_bad = nullptr, *d_outbad = nullptr, *d_status = nullptr;
   double *d_rin = nullptr, *d_zout = nullptr;  // host-pointer apply staging
   // pcg
@@ -345,6 +350,11 @@ extern "C" int ddmgnn_set_model(ddmgnn_ctx* c, int k_bar, int d, double alpha,
   PackedModel m;
   int st = pack_model(k_bar, d, alpha, params, n_params, &m, &err);
   if (st) return fail(st, err);
+  // layer 1 runs on h = 0: its h rows may be skipped when 0 * w = 0 exactly, i.e.
+  // when every weight of the slot is finite (else the reference's NaN must appear)
+  m.h0_finite = 1;
+  for (int i = 0; i < m.stride && i < static_cast<int>(m.bank.size()); ++i)
+    if (!std::isfinite(m.bank[i])) m.h0_finite = 0;
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(dalloc(&c->d_bank, m.bank.size()));
   CUDA_TRY(cudaMemcpy(c->d_bank, m.bank.data(), sizeof(float) * m.bank.size(),
@@ -361,8 +371,13 @@ extern "C" int ddmgnn_set_coarse_inverse(ddmgnn_ctx* c, int64_t k, const double*
   if (!c) return fail(kValueError, "null context");
   if (c->K && k != c->K) return fail(kValueError, "coarse size must equal the number of subdomains");
   CUDA_TRY(cudaSetDevice(c->device));
-  CUDA_TRY(dalloc(&c->d_cinv, static_cast<size_t>(k) * k));
-  CUDA_TRY(cudaMemcpy(c->d_cinv, inv, sizeof(double) * k * k, cudaMemcpyHostToDevice));
+  // rows padded to an even length (zero column) so the GEMV streams 16-byte loads
+  const int64_t ld = (k + 1) / 2 * 2;
+  CUDA_TRY(dalloc(&c->d_cinv, static_cast<size_t>(k) * ld));
+  CUDA_TRY(cudaMemset(c->d_cinv, 0, sizeof(double) * k * ld));
+  CUDA_TRY(cudaMemcpy2D(c->d_cinv, sizeof(double) * ld, inv, sizeof(double) * k,
+                        sizeof(double) * k, k, cudaMemcpyHostToDevice));
+  c->coarse_ld = static_cast<int>(ld);
   c->coarse_k = static_cast<int>(k);
   free_graphs(c);
   return kOk;
@@ -375,6 +390,9 @@ static int refresh_classes(ddmgnn_ctx* c) {
   if (!c->built || !c->have_model) return kOk;
   const int d = c->model.d;
   c->gnn_smem = gnn_plan_smem(d, c->lay.k_max, &c->cap0);
+  // DDMGNN_CAP0=<k>: route every subdomain larger than k to the cluster/flat paths
+  // (experiments: 0 sends all subdomains through the cluster path)
+  if (const char* e = getenv("DDMGNN_CAP0")) c->cap0 = std::min(c->cap0, atoi(e));
   const auto& sp = c->lay.h_sub_ptr;
   // oversized subdomains (k > cap0) lead the LPT order: those an 8-CTA cluster can
   // hold take the cluster path (smallest cluster size whose per-CTA share fits),
@@ -385,6 +403,10 @@ static int refresh_classes(ddmgnn_ctx* c) {
   // DSMEM traffic; profiles/r01_cluster_2cta_configE.jsonl), hence opt-in.
   const char* env = getenv("DDMGNN_CLUSTER");
   const bool use_cluster = !(env && env[0] == '0');
+  const char* env5 = getenv("DDMGNN_H0_SKIP");
+  c->h0_skip = !(env5 && env5[0] == '0');
+  const char* env4 = getenv("DDMGNN_FUSED_TAIL");
+  c->fused_tail = env4 && env4[0] == '1';
   const char* env3 = getenv("DDMGNN_TWO_CTA");
   c->two_cta = !(env3 && env3[0] == '0');
   const char* env2 = getenv("DDMGNN_CLUSTER_2CTA");
@@ -643,6 +665,7 @@ static cudaError_t enqueue_gnn_impl(ddmgnn_ctx* c, const double* r, int* status,
   a.bslices = c->d_bslices; a.n_bslices = c->n_bslices;
   a.csubs = c->d_csubs;
   a.two_cta = c->two_cta;
+  a.h0_skip = M.h0_finite && c->h0_skip;
   for (int j = 0; j < 3; ++j) {
     a.cluster_count[j] = c->cluster_count[j];
     a.cluster_smem[j] = c->cluster_smem[j];
@@ -694,7 +717,7 @@ static cudaError_t enqueue_apply(ddmgnn_ctx* c, const double* r, double* z, int 
   }
   if (e != cudaSuccess) return e;
   if (two) {
-    e = launch_coarse_gemv(c->K, c->d_cinv, c->d_r0r, c->d_y, skip, s);
+    e = launch_coarse_gemv(c->K, c->coarse_ld, c->d_cinv, c->d_r0r, c->d_y, skip, s);
     if (e != cudaSuccess) return e;
   }
   return launch_prolong(c->n, (two ? 1 : 0) | (asm_ ? 2 : 0), c->lay.tptr, c->lay.tent,
@@ -935,6 +958,23 @@ static cudaError_t enqueue_iteration(ddmgnn_ctx* c, int level, cudaStream_t s) {
   e = launch_update(n, c->d_u, c->d_r, c->d_p, c->d_q, c->d_partials, c->d_st, c->d_hist,
                     level == DDMGNN_PRECOND_NONE, s);
   if (e != cudaSuccess) return e;
+  const bool gnn = level == DDMGNN_LEVEL_ONE || level == DDMGNN_LEVEL_TWO;
+  const bool asm_ = level == DDMGNN_ASM_ONE || level == DDMGNN_ASM_TWO;
+  if ((gnn || asm_) && c->fused_tail) {
+    // local solves, then the fused tail: coarse GEMV + gluing + <r, z> + beta + p update
+    if (asm_) {
+      e = launch_asm_local(c->K, c->lay.k_max, c->lay.sub_ptr, c->lay.idx, c->d_ainv_off,
+                           c->d_ainv, c->lay.pou, c->d_r, c->d_zloc, c->d_r0r, c->d_scale, sw, s);
+    } else {
+      e = enqueue_gnn(c, c->d_r, sw, sw, s);
+    }
+    if (e != cudaSuccess) return e;
+    const bool two = level == DDMGNN_LEVEL_TWO || level == DDMGNN_ASM_TWO;
+    return launch_pcg_glue(n, (two ? 1 : 0) | (asm_ ? 2 : 0), c->K, c->coarse_ld, c->d_cinv,
+                           c->d_r0r, c->d_y,
+                           c->lay.tptr, c->lay.tent, c->lay.pou, c->d_scale, c->d_zloc, c->d_z,
+                           c->d_r, c->d_p, c->d_partials, c->d_st, s);
+  }
   if (level != DDMGNN_PRECOND_NONE) {
     e = enqueue_apply(c, c->d_r, c->d_z, level, sw, sw, 1, s);
     if (e != cudaSuccess) return e;

@@ -55,6 +55,11 @@ enum DevStatus : int {
 constexpr int kGnnThreads = GNN_THREADS;  // GNN CTA size (28 warps/SM; measured best of 640-1024)
 constexpr int kConstFloats = 16384;  // 64 KB constant bank
 constexpr int kFlatWarps = 8;        // slices (warps) per CTA of the flat path
+#ifndef GNN_EDGE_RELU_MAX
+// edge-loop relu as max(x, 0) on the ALU pipe (1) or 2 relu(x) = x + |x| on the FMA
+// pipe (0); the bank's message weights carry the matching factor (layout.cpp)
+#define GNN_EDGE_RELU_MAX 1
+#endif
 #ifndef GNN_Q2
 #define GNN_Q2 1  // phase A two slices per warp (shared weight loads; 2.4% faster)
 #endif
@@ -102,12 +107,15 @@ int build_host_layout(int n, const int64_t* indptr, const int32_t* indices, cons
 struct PackedModel {
   int k_bar = 0, d = 0, lmax = 0, stride = 0, dec_off = 0;
   float alpha = 0.f;
+  int h0_finite = 0;        // every weight of layer 1's bank slot is finite (h0 skip allowed)
   std::vector<float> bank;  // n_chunks * 16384 floats: chunk c = layers [c*lmax, ...)
   int n_chunks() const { return lmax ? (k_bar + lmax - 1) / lmax : 0; }
 };
 int gnn_supported_dim(int d);
 int gnn_lmax(int d);
 int gnn_stride(int d);
+// 1 when the kernels sum relu(x) over edges, 0 when they sum 2 relu(x) (GNN_EDGE_RELU_MAX)
+int gnn_edge_relu_plain();
 int gnn_smem_node_bytes(int d);
 int pack_model(int k_bar, int d, double alpha, const double* params, long long n_params,
                PackedModel* out, std::string* err);
@@ -144,6 +152,7 @@ struct GnnArgs {
   int n_bslices;
   const int* csubs;     // cluster path: subdomains of one cluster-size class
   int two_cta;           // CTA path: allow two CTAs per SM for small subdomains
+  int h0_skip;           // first chunk: layer 1 starts from h = 0 and its weights are finite
   int cluster_count[3];  // subdomains per cluster size 2, 4, 8 (csubs laid out in that order)
   int cluster_smem[3];   // dynamic shared memory per CTA of each cluster-size class
   int cluster_threads[3];  // threads per CTA (448 when two CTAs fit an SM, else kGnnThreads)
@@ -173,7 +182,7 @@ struct PcgState {
 };
 constexpr int kRedThreads = 256;
 int reduce_blocks(int n);
-cudaError_t launch_coarse_gemv(int K, const double* inv, const double* x, double* y,
+cudaError_t launch_coarse_gemv(int K, int ld, const double* inv, const double* x, double* y,
                                const int* skip, cudaStream_t s);
 cudaError_t launch_asm_local(int K, int k_max, const int* sub_ptr, const int* idx,
                              const long long* off, const double* ainv, const double* pou,
@@ -183,6 +192,12 @@ cudaError_t launch_prolong(int n, int two_level, const int* tptr, const int2* te
                            const double* pou, const double* y, const double* scale,
                            const double* zloc, double* z, const double* r, double* partials,
                            PcgState* st, int mode, const int* skip, cudaStream_t s);
+// Fused PCG tail after the local solves: coarse GEMV (two_level bit 0), gluing,
+// <r, z>, beta and p = z + beta p in one cooperative launch (krylov.cu).
+cudaError_t launch_pcg_glue(int n, int two_level, int K, int ld, const double* inv, const double* r0r,
+                            double* y, const int* tptr, const int2* tent, const double* pou,
+                            const double* scale, const double* zloc, double* z, const double* r,
+                            double* p, double* partials, PcgState* st, cudaStream_t s);
 // SELL-32 copy of A (built in set_matrix): slice q = rows 32q..32q+31, entry
 // (e, lane) at off[q] + 32 e + lane; padding entries have col = -1, val = 0.
 struct SellMatrix {

@@ -4,7 +4,12 @@
 #include "gnn_cfg.h"
 
 #ifndef DDM_GNN_DIMS
+#ifdef GNN_ONE_DIM  // experiment builds: one latent width only (make GNN_DIMS=<d>)
+#define DDM_ONE_DIM(X, d) X(d)
+#define DDM_GNN_DIMS(X) DDM_ONE_DIM(X, GNN_ONE_DIM)
+#else
 #define DDM_GNN_DIMS(X) X(3) X(4) X(5) X(10) X(20)
+#endif
 #endif
 
 namespace ddmgnn {
@@ -37,6 +42,8 @@ int gnn_lmax(int d) {
     default: return 0;
   }
 }
+int gnn_edge_relu_plain() { return GNN_EDGE_RELU_MAX ? 1 : 0; }
+
 int gnn_stride(int d) {
   switch (d) {
 #define X(DD) case DD: return Cfg<DD>::STRIDE;

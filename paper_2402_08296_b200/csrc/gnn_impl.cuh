@@ -97,10 +97,12 @@ __device__ __forceinline__ void store_vec(float* __restrict__ p, const float (&v
 // acc[j] += sum_m x[m] * W[m][2j:2j+2], W at bank offset base + OFF with row stride
 // RS.  `base` is warp-uniform (the layer's slot), so every weight pair is one
 // uniform-register-addressed constant load feeding a packed FFMA2.
-template <int NIN, int NPO, int OFF, int RS>
+// Rows m < M0 are skipped (their inputs are known to be exactly zero: the latent
+// state of the first layer, see H0 below).
+template <int NIN, int NPO, int OFF, int RS, int M0 = 0>
 __device__ __forceinline__ void mv2(int base, const float (&x)[NIN], float2 (&acc)[NPO]) {
 #pragma unroll
-  for (int m = 0; m < NIN; ++m) {
+  for (int m = M0; m < NIN; ++m) {
 #pragma unroll
     for (int j = 0; j < NPO; ++j)
       acc[j] = ffma2(bcast(x[m]), cpair(base + OFF + m * RS + 2 * j), acc[j]);
@@ -160,16 +162,28 @@ __device__ __forceinline__ void slice_q(int n0, int k, const float* h, float* q,
 
 // phase A for two slices at once (n0a, n0b): every weight pair loaded once feeds
 // both slices' FFMA2; the outputs are produced in two halves to bound registers.
-template <int D, int W>
+// H0: the latent state is exactly zero (first layer of a model, h = 0 after the
+// restriction, dss.py:309), so the h rows of every node mat-vec are skipped — the
+// host enables it only when those weights are finite, where 0 * w = 0 exactly.
+template <int D, int W, bool H0 = false>
 __device__ __forceinline__ void slice_q2(int n0a, int n0b, int k, const float* h, float* q,
                                          const float2* __restrict__ xy) {
   using C = Cfg<D>;
   constexpr int NP2 = C::NP2, H1 = NP2 / 2;
+  constexpr int M0 = H0 ? D : 0;
   const int lane = threadIdx.x & 31;
   const int na = min(n0a + lane, k - 1), nb = min(n0b + lane, k - 1);
   float xa[D + 2], xb[D + 2];
-  load_hxy<D>(h + na * C::HS, __ldg(xy + na), xa);
-  load_hxy<D>(h + nb * C::HS, __ldg(xy + nb), xb);
+  if constexpr (H0) {
+    const float2 pa = __ldg(xy + na), pb = __ldg(xy + nb);
+#pragma unroll
+    for (int i = 0; i < D; ++i) xa[i] = xb[i] = 0.f;
+    xa[D] = pa.x; xa[D + 1] = pa.y;
+    xb[D] = pb.x; xb[D + 1] = pb.y;
+  } else {
+    load_hxy<D>(h + na * C::HS, __ldg(xy + na), xa);
+    load_hxy<D>(h + nb * C::HS, __ldg(xy + nb), xb);
+  }
   float qsa[C::QS], qsb[C::QS];
 #pragma unroll
   for (int j = 0; j < C::QS; ++j) qsa[j] = qsb[j] = 0.f;
@@ -180,7 +194,7 @@ __device__ __forceinline__ void slice_q2(int n0a, int n0b, int k, const float* h
 #pragma unroll
     for (int j = 0; j < j1 - j0; ++j) aa[j] = ab[j] = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int m = 0; m < D + 2; ++m) {
+    for (int m = M0; m < D + 2; ++m) {
 #pragma unroll
       for (int j = j0; j < j1; ++j) {
         const float2 w = cpair(W + C::OFF_WQ + m * C::D2P + 2 * j);
@@ -209,7 +223,7 @@ struct LocalRows {
 
 // phase B: edge aggregation + node update; returns whether the lane's node became
 // non-finite and leaves the updated latent in hn (for a fused decoder)
-template <int D, int W, class Rows = LocalRows>
+template <int D, int W, class Rows = LocalRows, bool H0 = false>
 __device__ __forceinline__ bool slice_u(int n0, int k, float* h, Rows q,
                                         const float* c, const float2* __restrict__ xy,
                                         const float2* __restrict__ edges, int so, int width,
@@ -217,19 +231,28 @@ __device__ __forceinline__ bool slice_u(int n0, int k, float* h, Rows q,
                                         float (&hn)[Cfg<D>::DH], int kdummy = -1) {
   using C = Cfg<D>;
   constexpr int NP2 = C::NP2, NPH = C::NPH;
+  constexpr int M0 = H0 ? D : 0;  // first input row that can be non-zero
   const int lane = threadIdx.x & 31;
   const int n = n0 + lane;
   const int nn = min(n, k - 1);
   float2 p[NP2], s[NP2];
   {
     float hin[D + 2];
-    load_hxy<D>(h + nn * C::HS, __ldg(xy + nn), hin);
+    if constexpr (H0) {
+      const float2 pxy = __ldg(xy + nn);
+#pragma unroll
+      for (int i = 0; i < D; ++i) hin[i] = 0.f;
+      hin[D] = pxy.x;
+      hin[D + 1] = pxy.y;
+    } else {
+      load_hxy<D>(h + nn * C::HS, __ldg(xy + nn), hin);
+    }
 #pragma unroll
     for (int j = 0; j < NP2; ++j) {
       p[j] = cpair(W + C::OFF_B1 + 2 * j);
       s[j] = make_float2(0.f, 0.f);
     }
-    mv2<D + 2, NP2, W + C::OFF_WP, C::D2P>(0, hin, p);
+    mv2<D + 2, NP2, W + C::OFF_WP, C::D2P, M0>(0, hin, p);
   }
   const float2 dummy = make_float2(0.f, __int_as_float(kdummy < 0 ? k : kdummy));
   const float2* ep = edges + so + lane;
@@ -244,7 +267,13 @@ __device__ __forceinline__ bool slice_u(int n0, int k, float* h, Rows q,
     for (int j = 0; j < NP2; ++j) {
       float2 x = fadd2(p[j], make_float2(qt[2 * j], qt[2 * j + 1]));
       x = ffma2(len, cpair(W + C::OFF_WL + 2 * j), x);
+#if GNN_EDGE_RELU_MAX
+      // relu on the ALU pipe (FMNMX.NAN, NaN-propagating like numpy.maximum): the
+      // FMA pipe, which bounds the kernel, keeps 3 of the 4 packed ops per pair
+      s[j] = fadd2(s[j], make_float2(relu_nan(x.x), relu_nan(x.y)));
+#else
       s[j] = fadd2(s[j], relu2x(x));
+#endif
     }
   }
   // psi first layer with the messages' second layer folded in; the message part
@@ -252,10 +281,15 @@ __device__ __forceinline__ bool slice_u(int n0, int k, float* h, Rows q,
   float2 u[NPH], u2[NPH];
   float hc[D + 2];
   {
-    float hv[C::DH];
-    load_vec<C::DH>(h + nn * C::HS, hv);
+    if constexpr (H0) {
 #pragma unroll
-    for (int i = 0; i < D; ++i) hc[i] = hv[i];
+      for (int i = 0; i < D; ++i) hc[i] = 0.f;
+    } else {
+      float hv[C::DH];
+      load_vec<C::DH>(h + nn * C::HS, hv);
+#pragma unroll
+      for (int i = 0; i < D; ++i) hc[i] = hv[i];
+    }
     hc[D] = c[nn];
     hc[D + 1] = static_cast<float>(deg[nn]);
   }
@@ -264,7 +298,7 @@ __device__ __forceinline__ bool slice_u(int n0, int k, float* h, Rows q,
     u[j] = cpair(W + C::OFF_BP1 + 2 * j);
     u2[j] = make_float2(0.f, 0.f);
   }
-  mv2<D + 2, NPH, W + C::OFF_WU, C::DP>(0, hc, u);
+  mv2<D + 2, NPH, W + C::OFF_WU, C::DP, M0>(0, hc, u);
   {
     float sv[2 * D];
 #pragma unroll
@@ -679,7 +713,11 @@ __device__ __forceinline__ void tc_layer(const SmemState<D>& ns, int k, int warp
         for (int j = 0; j < NP2; ++j) {
           float2 x = fadd2(p[j], make_float2(qt[2 * j], qt[2 * j + 1]));
           x = ffma2(len, cpair(W + C::OFF_WL + 2 * j), x);
+#if GNN_EDGE_RELU_MAX
+          s[j] = fadd2(s[j], make_float2(relu_nan(x.x), relu_nan(x.y)));
+#else
           s[j] = fadd2(s[j], relu2x(x));
+#endif
         }
       }
     }
@@ -742,7 +780,7 @@ __device__ __forceinline__ void tc_layer(const SmemState<D>& ns, int k, int warp
 #endif
 
 // one layer, all slices of the CTA's subdomain (warp w: slices w, w + nwarps, ...)
-template <int D, int W>
+template <int D, int W, bool H0 = false>
 __device__ __forceinline__ void cta_layer(const SmemState<D>& ns, int k, int warp,
                                           const float2* xy, const float2* edges,
                                           const int* slice_off, const uint16_t* deg,
@@ -762,7 +800,7 @@ __device__ __forceinline__ void cta_layer(const SmemState<D>& ns, int k, int war
     const int nsl = (k + 31) >> 5, half = (nsl + 1) >> 1;
     for (int sa = warp; sa < half; sa += step >> 5) {
       const int sb = sa + half < nsl ? sa + half : sa;  // odd count: last pair repeats sa
-      slice_q2<D, W>(sa * 32, sb * 32, k, ns.h, ns.q, xy);
+      slice_q2<D, W, H0>(sa * 32, sb * 32, k, ns.h, ns.q, xy);
     }
   }
 #else
@@ -775,8 +813,8 @@ __device__ __forceinline__ void cta_layer(const SmemState<D>& ns, int k, int war
     const int so = uni(slice_off[n0 >> 5]);
     const int width = (uni(slice_off[(n0 >> 5) + 1]) - so) >> 5;
     float hn[Cfg<D>::DH];
-    const bool b = slice_u<D, W>(n0, k, ns.h, LocalRows{ns.q}, ns.c, xy, edges, so, width, deg,
-                                 alpha, hn);
+    const bool b = slice_u<D, W, LocalRows, H0>(n0, k, ns.h, LocalRows{ns.q}, ns.c, xy, edges,
+                                                so, width, deg, alpha, hn);
     if (b && first_bad == 0) first_bad = layer_no;
   }
   if (first_bad != 0) atomicCAS(bad, 0, first_bad);  // first bad layer wins
@@ -914,7 +952,19 @@ __global__ void __launch_bounds__(gnn_cta_threads<D>(), 1) gnn_kernel(GnnArgs a)
       cta_layer<D, LL * C::STRIDE>(ns, k, warp, xy, a.edges, so, dg, a.alpha, &sh.bad,       \
                                    a.layer0 + LL, tmem, sh.mbar, uses);                      \
   }
-    DDM_LAYER(0) DDM_LAYER(1) DDM_LAYER(2) DDM_LAYER(3) DDM_LAYER(4)
+#if !GNN_TC_Q
+    // the first layer of the model starts from h = 0 (dss.py:309)
+    if (a.first && a.h0_skip) {
+      if (a.nl > 0)
+        cta_layer<D, 0, true>(ns, k, warp, xy, a.edges, so, dg, a.alpha, &sh.bad, a.layer0, tmem,
+                              sh.mbar, uses);
+    } else {
+      DDM_LAYER(0)
+    }
+#else
+    DDM_LAYER(0)
+#endif
+    DDM_LAYER(1) DDM_LAYER(2) DDM_LAYER(3) DDM_LAYER(4)
     DDM_LAYER(5) DDM_LAYER(6) DDM_LAYER(7) DDM_LAYER(8) DDM_LAYER(9)
 #undef DDM_LAYER
   }

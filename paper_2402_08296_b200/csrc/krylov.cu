@@ -14,7 +14,11 @@
 // reference's sequential order, so given equal inputs they are bit-identical to
 // scipy.  Dot products use a deterministic two-stage tree reduction (fixed grid,
 // fixed order), which differs from BLAS ddot only by summation order.
+#include <cooperative_groups.h>
+
+#include <algorithm>
 #include <cmath>
+#include <cstdint>
 
 #include "ddmgnn_internal.h"
 
@@ -163,6 +167,12 @@ cudaError_t launch_spmv_pq(const SellMatrix& m, const double* p, double* q, doub
 }
 
 // ------------------------------------------------------------------ BLAS-1
+// Vector kernels stream 16-byte (double2) loads, several per thread in flight,
+// when the vectors are 16-byte aligned (the context's own buffers always are).
+__device__ __forceinline__ bool aligned16(const void* p) {
+  return (reinterpret_cast<uintptr_t>(p) & 15) == 0;
+}
+
 __global__ void __launch_bounds__(kRedThreads) update_kernel(int n, double* __restrict__ u,
                                                              double* __restrict__ r,
                                                              const double* __restrict__ p,
@@ -174,7 +184,33 @@ __global__ void __launch_bounds__(kRedThreads) update_kernel(int n, double* __re
   // plain flexible CG (z = r): beta = <r', r' - r> / rho needs <r', r>
   const bool flex_id = identity && st->flexible;
   double rr = 0.0, rro = 0.0;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+  int j_scalar = 0;
+  if (aligned16(u) && aligned16(r) && aligned16(p) && aligned16(q)) {
+    const int n2 = n >> 1;
+    double2* u2 = reinterpret_cast<double2*>(u);
+    double2* r2 = reinterpret_cast<double2*>(r);
+    const double2* p2 = reinterpret_cast<const double2*>(p);
+    const double2* q2 = reinterpret_cast<const double2*>(q);
+    for (int i = tid; i < n2; i += stride) {
+      const double2 uo = u2[i], ro = r2[i], pp = __ldg(p2 + i), qq = __ldg(q2 + i);
+      double2 un, rn;
+      un.x = __dadd_rn(uo.x, __dmul_rn(alpha, pp.x));  // sparse.py:112
+      un.y = __dadd_rn(uo.y, __dmul_rn(alpha, pp.y));
+      rn.x = __dsub_rn(ro.x, __dmul_rn(alpha, qq.x));  // sparse.py:113
+      rn.y = __dsub_rn(ro.y, __dmul_rn(alpha, qq.y));
+      u2[i] = un;
+      r2[i] = rn;
+      rr += rn.x * rn.x;
+      rr += rn.y * rn.y;
+      if (flex_id) {
+        rro += rn.x * __dsub_rn(rn.x, ro.x);
+        rro += rn.y * __dsub_rn(rn.y, ro.y);
+      }
+    }
+    j_scalar = 2 * n2;
+  }
+  for (int j = j_scalar + tid; j < n; j += stride) {
     u[j] = __dadd_rn(u[j], __dmul_rn(alpha, p[j]));  // sparse.py:112
     const double r_old = r[j];
     const double rj = __dsub_rn(r_old, __dmul_rn(alpha, q[j]));  // sparse.py:113
@@ -218,7 +254,20 @@ __global__ void __launch_bounds__(kRedThreads) pupdate_kernel(int n, double* __r
                                                               const PcgState* st) {
   if (st->status != kRunning) return;
   const double beta = st->beta;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+  int j_scalar = 0;
+  if (aligned16(p) && aligned16(z)) {
+    const int n2 = n >> 1;
+    double2* p2 = reinterpret_cast<double2*>(p);
+    const double2* z2 = reinterpret_cast<const double2*>(z);
+    for (int i = tid; i < n2; i += stride) {
+      const double2 pp = p2[i], zz = __ldg(z2 + i);
+      p2[i] = make_double2(__dadd_rn(zz.x, __dmul_rn(beta, pp.x)),  // sparse.py:126
+                           __dadd_rn(zz.y, __dmul_rn(beta, pp.y)));
+    }
+    j_scalar = 2 * n2;
+  }
+  for (int j = j_scalar + tid; j < n; j += stride)
     p[j] = __dadd_rn(z[j], __dmul_rn(beta, p[j]));  // sparse.py:126
 }
 
@@ -298,7 +347,28 @@ __global__ void __launch_bounds__(kRedThreads) rz_beta_kernel(int n, const doubl
   if (st->status != kRunning) return;
   const bool flex = st->flexible && zold != nullptr;
   double rz = 0.0, rzo = 0.0;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+  // same element-to-thread map and per-thread order as update_kernel's ||r||^2, so
+  // that PCG with the identity operator reproduces CG bit for bit (test_sparse.py:60-66)
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+  int j_scalar = 0;
+  if (aligned16(r) && aligned16(z) && (zold == nullptr || aligned16(zold))) {
+    const int n2 = n >> 1;
+    const double2* r2 = reinterpret_cast<const double2*>(r);
+    const double2* z2 = reinterpret_cast<const double2*>(z);
+    const double2* o2 = reinterpret_cast<const double2*>(zold);
+    for (int i = tid; i < n2; i += stride) {
+      const double2 rr = r2[i], zz = z2[i];
+      rz += rr.x * zz.x;
+      rz += rr.y * zz.y;
+      if (flex) {
+        const double2 oo = o2[i];
+        rzo += rr.x * __dsub_rn(zz.x, oo.x);
+        rzo += rr.y * __dsub_rn(zz.y, oo.y);
+      }
+    }
+    j_scalar = 2 * n2;
+  }
+  for (int j = j_scalar + tid; j < n; j += stride) {
     const double rj = r[j], zj = z[j];
     rz += rj * zj;
     if (flex) rzo += rj * __dsub_rn(zj, zold[j]);
@@ -329,12 +399,14 @@ cudaError_t launch_copy(int n, const double* src, double* dst, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ coarse level
-// y = inv(R0 A R0^T) x (fp64, row-major inverse), 128 threads (4 warps) per row and
-// two rows per block so ~K/2 blocks keep enough loads in flight for the 8 K^2
-// byte stream (a warp per row left it latency bound).  Fixed reduction order.
-// Replaces the dense LU solve of sparse.py:163 (coarse matrix factorised at setup).
+// y = inv(R0 A R0^T) x (fp64, row-major inverse with leading dimension ld), 128
+// threads (4 warps) per row and two rows per block so ~K/2 blocks keep the 8 K^2
+// byte stream in flight; with an even ld (the context pads its copy) every thread
+// issues its 16-byte row loads back to back.  Fixed reduction order.  Replaces
+// the dense LU solve of sparse.py:163 (coarse matrix factorised at setup).
 constexpr int kGemvRowThreads = 128;
-__global__ void __launch_bounds__(256) coarse_gemv_kernel(int K, const double* __restrict__ inv,
+__global__ void __launch_bounds__(256) coarse_gemv_kernel(int K, int ld,
+                                                          const double* __restrict__ inv,
                                                           const double* __restrict__ x,
                                                           double* __restrict__ y,
                                                           const int* skip) {
@@ -345,18 +417,39 @@ __global__ void __launch_bounds__(256) coarse_gemv_kernel(int K, const double* _
   const int row = blockIdx.x * 2 + half;
   double acc = 0.0;
   if (row < K) {
-    const double* rp = inv + static_cast<size_t>(row) * K;
-    int j = t;
-    for (; j + 3 * kGemvRowThreads < K; j += 4 * kGemvRowThreads) {
-      const double a0 = __ldcs(&rp[j]), a1 = __ldcs(&rp[j + kGemvRowThreads]);
-      const double a2 = __ldcs(&rp[j + 2 * kGemvRowThreads]);
-      const double a3 = __ldcs(&rp[j + 3 * kGemvRowThreads]);
-      acc = fma(a0, __ldg(&x[j]), acc);
-      acc = fma(a1, __ldg(&x[j + kGemvRowThreads]), acc);
-      acc = fma(a2, __ldg(&x[j + 2 * kGemvRowThreads]), acc);
-      acc = fma(a3, __ldg(&x[j + 3 * kGemvRowThreads]), acc);
+    // thread t takes column pairs (2j, 2j+1), j = t, t + 128, ... in this order
+    // whatever the alignment (16-byte loads when possible), so the result does not
+    // depend on ld or on where the matrix lives (sharded solve: bit-identical z)
+    const double* rp = inv + static_cast<size_t>(row) * ld;
+    const int k2 = K >> 1;
+    if ((ld & 1) == 0 && aligned16(inv) && aligned16(x)) {
+      const double2* r2 = reinterpret_cast<const double2*>(rp);
+      const double2* x2 = reinterpret_cast<const double2*>(x);
+      int j = t;
+      for (; j + 3 * kGemvRowThreads < k2; j += 4 * kGemvRowThreads) {
+        const double2 a0 = __ldcs(r2 + j), a1 = __ldcs(r2 + j + kGemvRowThreads);
+        const double2 a2 = __ldcs(r2 + j + 2 * kGemvRowThreads);
+        const double2 a3 = __ldcs(r2 + j + 3 * kGemvRowThreads);
+        const double2 b0 = __ldg(x2 + j), b1 = __ldg(x2 + j + kGemvRowThreads);
+        const double2 b2 = __ldg(x2 + j + 2 * kGemvRowThreads);
+        const double2 b3 = __ldg(x2 + j + 3 * kGemvRowThreads);
+        acc = fma(a0.x, b0.x, acc); acc = fma(a0.y, b0.y, acc);
+        acc = fma(a1.x, b1.x, acc); acc = fma(a1.y, b1.y, acc);
+        acc = fma(a2.x, b2.x, acc); acc = fma(a2.y, b2.y, acc);
+        acc = fma(a3.x, b3.x, acc); acc = fma(a3.y, b3.y, acc);
+      }
+      for (; j < k2; j += kGemvRowThreads) {
+        const double2 a0 = __ldcs(r2 + j), b0 = __ldg(x2 + j);
+        acc = fma(a0.x, b0.x, acc);
+        acc = fma(a0.y, b0.y, acc);
+      }
+    } else {
+      for (int j = t; j < k2; j += kGemvRowThreads) {
+        acc = fma(__ldcs(rp + 2 * j), __ldg(x + 2 * j), acc);
+        acc = fma(__ldcs(rp + 2 * j + 1), __ldg(x + 2 * j + 1), acc);
+      }
     }
-    for (; j < K; j += kGemvRowThreads) acc = fma(__ldcs(&rp[j]), __ldg(&x[j]), acc);
+    if ((K & 1) && t == 0) acc = fma(__ldcs(rp + K - 1), __ldg(x + K - 1), acc);
   }
   acc = warp_sum_d(acc);
   if ((threadIdx.x & 31) == 0) part[half][t >> 5] = acc;
@@ -369,9 +462,9 @@ __global__ void __launch_bounds__(256) coarse_gemv_kernel(int K, const double* _
   }
 }
 
-cudaError_t launch_coarse_gemv(int K, const double* inv, const double* x, double* y,
+cudaError_t launch_coarse_gemv(int K, int ld, const double* inv, const double* x, double* y,
                                const int* skip, cudaStream_t s) {
-  coarse_gemv_kernel<<<(K + 1) / 2, 2 * kGemvRowThreads, 0, s>>>(K, inv, x, y, skip);
+  coarse_gemv_kernel<<<(K + 1) / 2, 2 * kGemvRowThreads, 0, s>>>(K, ld, inv, x, y, skip);
   return cudaGetLastError();
 }
 
@@ -439,7 +532,39 @@ cudaError_t launch_asm_local(int K, int k_max, const int* sub_ptr, const int* id
 }
 
 // ------------------------------------------------------------------ prolongation
+// z_j of DOF j (hybrid.py:117,133-135 / asm.py:108-113) over the transpose map.
 // two_level bit 0: add the coarse correction; bit 1: ASM order (local terms first).
+__device__ __forceinline__ double glue_dof(int j, int two_level, const int* __restrict__ tptr,
+                                           const int2* __restrict__ tent,
+                                           const double* __restrict__ pou,
+                                           const double* __restrict__ y,
+                                           const double* __restrict__ scale,
+                                           const double* __restrict__ zloc) {
+  const int b = tptr[j], e = tptr[j + 1];
+  double acc = 0.0;
+  if (two_level & 2) {
+    // ASM order (asm.py:108-113): local sum first, coarse correction added last
+    for (int t = b; t < e; ++t) acc = __dadd_rn(acc, zloc[tent[t].x]);
+    if (two_level & 1) {
+      const double w = pou[j];
+      double c = 0.0;
+      for (int t = b; t < e; ++t) c = __dadd_rn(c, __dmul_rn(w, y[tent[t].y]));
+      acc = __dadd_rn(acc, c);
+    }
+  } else {
+    if (two_level) {  // z = r0.T @ y  (CSC matvec order: ascending subdomain)
+      const double w = pou[j];
+      for (int t = b; t < e; ++t) acc = __dadd_rn(acc, __dmul_rn(w, y[tent[t].y]));
+    }
+    for (int t = b; t < e; ++t) {  // z[idx_i] += s_i * sol_i, ascending i (hybrid.py:134-135)
+      const int2 pe = tent[t];
+      if (scale[pe.y] != 0.0) acc = __dadd_rn(acc, zloc[pe.x]);
+    }
+  }
+  return acc;
+}
+
+
 // mode 0: plain apply.  mode 1: PCG — also <r, z> -> rho', beta (sparse.py:123-125).
 __global__ void __launch_bounds__(kRedThreads) prolong_kernel(
     int n, int two_level, const int* __restrict__ tptr, const int2* __restrict__ tent,
@@ -451,27 +576,7 @@ __global__ void __launch_bounds__(kRedThreads) prolong_kernel(
   const bool flex = mode == 1 && st->flexible;
   double rz = 0.0, rzo = 0.0;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    const int b = tptr[j], e = tptr[j + 1];
-    double acc = 0.0;
-    if (two_level & 2) {
-      // ASM order (asm.py:108-113): local sum first, coarse correction added last
-      for (int t = b; t < e; ++t) acc = __dadd_rn(acc, zloc[tent[t].x]);
-      if (two_level & 1) {
-        const double w = pou[j];
-        double c = 0.0;
-        for (int t = b; t < e; ++t) c = __dadd_rn(c, __dmul_rn(w, y[tent[t].y]));
-        acc = __dadd_rn(acc, c);
-      }
-    } else {
-      if (two_level) {  // z = r0.T @ y  (CSC matvec order: ascending subdomain)
-        const double w = pou[j];
-        for (int t = b; t < e; ++t) acc = __dadd_rn(acc, __dmul_rn(w, y[tent[t].y]));
-      }
-      for (int t = b; t < e; ++t) {  // z[idx_i] += s_i * sol_i, ascending i (hybrid.py:134-135)
-        const int2 pe = tent[t];
-        if (scale[pe.y] != 0.0) acc = __dadd_rn(acc, zloc[pe.x]);
-      }
-    }
+    const double acc = glue_dof(j, two_level, tptr, tent, pou, y, scale, zloc);
     if (mode == 1) {
       const double rj = r[j];
       rz += rj * acc;
@@ -499,6 +604,171 @@ cudaError_t launch_prolong(int n, int two_level, const int* tptr, const int2* te
                                                           scale, zloc, z, r, partials, st, mode,
                                                           skip);
   return cudaGetLastError();
+}
+
+
+// ------------------------------------------------------------------ fused PCG tail
+// Everything of one PCG iteration after the local solves (sparse.py:122-126 with
+// hybrid.py:117,133-135) in ONE cooperative launch, two grid-wide barriers:
+//   1. y = inv(R0 A R0^T) (R0 r)   (coarse GEMV, block per row, 16-byte loads)
+//   2. z_j = glue (transpose map), <r, z> (+ <r, z - z_old>): block partials
+//   3. every block sums the partials in block order (identical bits everywhere),
+//      beta = rho'/rho (or Polak-Ribiere), p_j = z_j + beta p_j with z_j kept in
+//      registers (up to kGlueRegs DOFs per thread; beyond that z is re-read).
+// z is stored only when something reads it later (flexible CG's z_old, or the
+// register budget).  Replaces coarse_gemv_kernel + prolong_kernel (mode 1) +
+// pupdate_kernel: two launches and the z round trip through HBM.
+constexpr int kGlueRegs = 8;
+
+struct GlueArgs {
+  int n, two_level, K, ld;
+  const int* tptr;
+  const int2* tent;
+  const double *pou, *inv, *r0r, *scale, *zloc, *r;
+  double *y, *z, *p, *partials;
+  PcgState* st;
+};
+
+__global__ void __launch_bounds__(kRedThreads) pcg_glue_kernel(GlueArgs a) {
+  namespace cg = cooperative_groups;
+  PcgState* st = a.st;
+  if (st->status != kRunning) return;  // same value in every block: no barrier is skipped
+  cg::grid_group grid = cg::this_grid();
+  const double rho = st->rho;          // read before block 0 replaces it
+  const bool flex = st->flexible != 0;
+  __shared__ double red[2][kRedThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // 1. coarse GEMV
+  if (a.two_level & 1) {
+    const int K = a.K;
+    for (int row = blockIdx.x; row < K; row += gridDim.x) {
+      const double* rp = a.inv + static_cast<size_t>(row) * a.ld;
+      double acc = 0.0;
+      if ((K & 1) == 0 && (a.ld & 1) == 0) {  // rows 16-byte aligned
+        const double2* rp2 = reinterpret_cast<const double2*>(rp);
+        const double2* x2 = reinterpret_cast<const double2*>(a.r0r);
+        for (int j = threadIdx.x; j < K / 2; j += blockDim.x) {
+          const double2 m = __ldcs(rp2 + j), x = __ldg(x2 + j);
+          acc = fma(m.x, x.x, acc);
+          acc = fma(m.y, x.y, acc);
+        }
+      } else {
+        for (int j = threadIdx.x; j < K; j += blockDim.x) acc = fma(__ldcs(rp + j), __ldg(a.r0r + j), acc);
+      }
+      acc = warp_sum_d(acc);
+      if (lane == 0) red[0][warp] = acc;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (blockDim.x >> 5); ++w) t += red[0][w];
+        a.y[row] = t;
+      }
+      __syncthreads();
+    }
+    grid.sync();
+  }
+  // 2. gluing + <r, z>
+  const int stride = gridDim.x * blockDim.x;
+  const int j0 = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool in_regs = (a.n + stride - 1) / stride <= kGlueRegs;
+  const bool store_z = flex || !in_regs;
+  double zr[kGlueRegs];
+  double rz = 0.0, rzo = 0.0;
+#pragma unroll
+  for (int m = 0; m < kGlueRegs; ++m) zr[m] = 0.0;
+  {
+    int m = 0;
+    for (int j = j0; j < a.n; j += stride, ++m) {
+      const double zj = glue_dof(j, a.two_level, a.tptr, a.tent, a.pou, a.y, a.scale, a.zloc);
+      const double rj = a.r[j];
+      rz += rj * zj;
+      if (flex) rzo += rj * __dsub_rn(zj, a.z[j]);  // z still holds z_old
+#pragma unroll
+      for (int q = 0; q < kGlueRegs; ++q)
+        if (q == m) zr[q] = zj;
+      if (store_z) a.z[j] = zj;
+    }
+  }
+  rz = warp_sum_d(rz);
+  rzo = warp_sum_d(rzo);
+  if (lane == 0) {
+    red[0][warp] = rz;
+    red[1][warp] = rzo;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t0 = 0.0, t1 = 0.0;
+    for (int w = 0; w < (blockDim.x >> 5); ++w) {
+      t0 += red[0][w];
+      t1 += red[1][w];
+    }
+    a.partials[2 * blockIdx.x] = t0;
+    a.partials[2 * blockIdx.x + 1] = t1;
+  }
+  grid.sync();
+  // 3. totals in block order (every block the same), beta, p update
+  __shared__ double tot[2];
+  if (warp == 0) {
+    double t0 = 0.0, t1 = 0.0;
+    for (int b = lane; b < static_cast<int>(gridDim.x); b += 32) {
+      t0 += __ldcg(&a.partials[2 * b]);
+      t1 += __ldcg(&a.partials[2 * b + 1]);
+    }
+    t0 = warp_sum_d(t0);
+    t1 = warp_sum_d(t1);
+    if (lane == 0) {
+      tot[0] = t0;
+      tot[1] = t1;
+    }
+  }
+  __syncthreads();
+  const double beta = (flex ? tot[1] : tot[0]) / rho;  // sparse.py:124 (or Polak-Ribiere)
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->rz = tot[0];
+    st->rzo = tot[1];
+    st->beta = beta;
+    st->rho = tot[0];  // sparse.py:125
+  }
+  {
+    int m = 0;
+    for (int j = j0; j < a.n; j += stride, ++m) {
+      double zj = 0.0;
+      if (in_regs) {
+#pragma unroll
+        for (int q = 0; q < kGlueRegs; ++q)
+          if (q == m) zj = zr[q];
+      } else {
+        zj = a.z[j];
+      }
+      a.p[j] = __dadd_rn(zj, __dmul_rn(beta, a.p[j]));  // sparse.py:126
+    }
+  }
+}
+
+cudaError_t launch_pcg_glue(int n, int two_level, int K, int ld, const double* inv, const double* r0r,
+                            double* y, const int* tptr, const int2* tent, const double* pou,
+                            const double* scale, const double* zloc, double* z, const double* r,
+                            double* p, double* partials, PcgState* st, cudaStream_t s) {
+  static int max_blocks = 0;
+  if (max_blocks == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_glue_kernel, kRedThreads, 0);
+    max_blocks = std::max(1, std::min(kMaxRedBlocks, sms * per_sm));
+  }
+  GlueArgs a{n, two_level, K, ld, tptr, tent, pou, inv, r0r, scale, zloc, r, y, z, p, partials, st};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(std::min(max_blocks, std::max(reduce_blocks(n), two_level & 1 ? K : 1)));
+  cfg.blockDim = dim3(kRedThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, pcg_glue_kernel, a);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace ddmgnn

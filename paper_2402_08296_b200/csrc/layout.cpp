@@ -226,9 +226,10 @@ int build_host_layout(int n, const int64_t* indptr, const int32_t* indices, cons
 //   b1  [2d], WL [2d] = W1cat |d| row
 //   WU  [3d+2][d]  = [Wp1 h rows ; Wp1 c row ; bdeg ; Mo ; Mi]
 //         bdeg = b2o . Wp1[phi_o rows] + b2i . Wp1[phi_i rows]      (x node degree)
-//         Mo   = 0.5 * W2o . Wp1[phi_o rows],  Mi = 0.5 * W2i . Wp1[phi_i rows]
+//         Mo   = e * W2o . Wp1[phi_o rows],  Mi = e * W2i . Wp1[phi_i rows]
 //   bp1 [d], WP2 [d][d] = 0.5 * Wp2, bp2 [d]
-// (the 0.5 factors pair with the kernel's relu(x) = (x + |x|) / 2).  The folded
+// (WP2's 0.5 pairs with the kernel's node relu(x) = (x + |x|) / 2; e = 1 when the
+// edge loop sums max(x, 0), 0.5 when it sums x + |x|, gnn_edge_relu_plain()).  The folded
 // products are formed in fp64 and rounded once.  The FINAL layer's decoder
 // (dss.py:327; only the last output is consumed by hybrid.py:124) sits at the end
 // of every bank: Wd1[d][d] bd1[d] wd2[d] bd2.
@@ -303,6 +304,7 @@ int pack_model(int k_bar, int d, double alpha, const double* params, long long n
     }
     // psi first layer (3D+1 inputs [h, c, phi_o, phi_i], dss.py:293-299) with the
     // messages' second layer folded in
+    const double edge_scale = gnn_edge_relu_plain() ? 1.0 : 0.5;
     const double* wp1_o = wp1 + (D + 1) * D;      // rows of phi_o
     const double* wp1_i = wp1 + (2 * D + 1) * D;  // rows of phi_i
     for (int j = 0; j < D; ++j) {
@@ -316,8 +318,8 @@ int pack_model(int k_bar, int d, double alpha, const double* params, long long n
           mo += w2o[m * D + q] * wp1_o[q * D + j];
           mi += w2i[m * D + q] * wp1_i[q * D + j];
         }
-        B[o[WU] + (D + 2 + m) * dp + j] = f(0.5 * mo);
-        B[o[WU] + (2 * D + 2 + m) * dp + j] = f(0.5 * mi);
+        B[o[WU] + (D + 2 + m) * dp + j] = f(edge_scale * mo);
+        B[o[WU] + (2 * D + 2 + m) * dp + j] = f(edge_scale * mi);
       }
       B[o[BP1] + j] = f(bp1[j]);
       B[o[BP2] + j] = f(bp2[j]);

@@ -12,7 +12,9 @@
 //
 // Vector kernels here are HBM-bound fp64 streams; dot products use a fixed
 // two-stage reduction (deterministic for a given n).
+#include <algorithm>
 #include <cmath>
+#include <cstring>
 
 #include "../../include/ddmgnn_b200.h"
 #include "ddmgnn_internal.h"
@@ -176,7 +178,7 @@ extern "C" int ddmgnn_xpby(int64_t n, const double* z, double beta, double* p, v
 extern "C" int ddmgnn_dense_gemv(int64_t k, const double* a, const double* x, double* y,
                                  void* stream) {
   if (k <= 0) return 0;
-  return cuda_status(launch_coarse_gemv(static_cast<int>(k), a, x, y, nullptr,
+  return cuda_status(launch_coarse_gemv(static_cast<int>(k), static_cast<int>(k), a, x, y, nullptr,
                                         static_cast<cudaStream_t>(stream)));
 }
 
@@ -278,3 +280,281 @@ extern "C" int ddmgnn_xpby_dev(int64_t n, const double* z, const double* st, dou
   xpby_dev_kernel<<<nblocks(n), kT, 0, static_cast<cudaStream_t>(stream)>>>(n, z, st, p);
   return cuda_status(cudaGetLastError());
 }
+
+// ---------------------------------------------------------------- peer collectives
+// Device-resident exchanges between the ranks' GPUs over peer memory (CUDA IPC
+// mappings; NVLink/NVSwitch between the GPUs of one box), ordered by device flags
+// only, so every call is stream-ordered and graph-capturable (no host barrier).
+// Every rank owns a flag block int64[DDMGNN_PEER_FLAG_WORDS] (zeroed, mapped by all);
+// channel c occupies words [32 c, 32 c + 32):
+//   sig[h]  (+0..7)   epoch of the last message rank h delivered to this rank
+//   ack[h]  (+8..15)  epoch of the last message of this rank that rank h consumed
+//   ctr     (+16)     this rank's epoch counter of the channel (bumped by the sender side)
+//   done[h] (+17..24) block-completion counters of the multi-block kernels
+//   fin     (+25)     completion counter over all destination slices
+// Every rank makes the same sequence of calls per channel, so the counters agree.
+// Before overwriting a peer's receive buffer with epoch e the sender waits for the
+// peer's acknowledgement of e - 1; the receiver acknowledges after consuming.
+namespace ddmgnn {
+namespace {
+
+constexpr int kPeerMax = DDMGNN_PEER_MAX;
+constexpr int kChanWords = 32;
+enum { kSig = 0, kAck = 8, kCtr = 16, kDone = 17, kFin = 25 };
+constexpr int kErrWord = DDMGNN_PEER_FLAG_WORDS - 1;  // in channel 7's spare words
+
+struct PeerArgs {
+  long long* flags[kPeerMax];  // rank h's flag block (this rank's own at [me])
+  double* buf[kPeerMax];       // per-rank destination base (put: receive buffer of h)
+  long long off[kPeerMax + 1]; // segment offsets (send side: into idx; recv side: into recv)
+  long long doff[kPeerMax];    // put: offset of this rank's segment in h's receive buffer
+  int g, me, chan;
+};
+
+__device__ __forceinline__ long long ld_acq(const long long* p) {
+  long long v;
+  asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_rel(long long* p, long long v) {
+  asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// Spin until *p >= v.  A peer that never arrives (a rank that died or diverged)
+// does not hang the GPU: after kPeerTimeoutNs the wait gives up and raises the
+// rank's error word (flags[kErrWord]), which the host checks at its status polls.
+constexpr unsigned long long kPeerTimeoutNs = 30ull * 1000 * 1000 * 1000;
+__device__ __forceinline__ void wait_geq(const long long* p, long long v, long long* err) {
+  if (ld_acq(p) >= v) return;
+  const unsigned long long t0 = globaltimer();
+  while (ld_acq(p) < v) {
+    __nanosleep(200);
+    if (globaltimer() - t0 > kPeerTimeoutNs) {
+      atomicExch(reinterpret_cast<unsigned long long*>(err), 1ull);
+      return;
+    }
+  }
+}
+__device__ __forceinline__ long long* chan_of(const PeerArgs& a, int h) {
+  return a.flags[h] + a.chan * kChanWords;
+}
+
+// grid (x blocks, g slices): slice h copies src[idx[off[h] .. off[h+1])] into
+// buf[h] + doff[h]; the last block of a slice signals h; the last slice bumps ctr.
+__global__ void __launch_bounds__(kT) peer_put_kernel(const double* __restrict__ src,
+                                                       const int* __restrict__ idx, PeerArgs a) {
+  long long* my = chan_of(a, a.me);
+  const int h = blockIdx.y;
+  const long long b0 = a.off[h], cnt = a.off[h + 1] - b0;
+  const long long e = ld_acq(my + kCtr) + 1;
+  const bool send = cnt > 0 && h != a.me;
+  if (send) {
+    if (threadIdx.x == 0) wait_geq(my + kAck + h, e - 1, a.flags[a.me] + kErrWord);  // h consumed e - 1
+    __syncthreads();
+    double* dst = a.buf[h] + a.doff[h];
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < cnt;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+      dst[i] = src[idx[b0 + i]];
+    __threadfence_system();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long d =
+        atomicAdd(reinterpret_cast<unsigned long long*>(my + kDone + h), 1ull);
+    if (d == gridDim.x - 1) {  // last block of slice h
+      my[kDone + h] = 0;
+      if (send) {
+        __threadfence_system();
+        st_rel(chan_of(a, h) + kSig + a.me, e);
+      }
+      __threadfence();
+      const unsigned long long f =
+          atomicAdd(reinterpret_cast<unsigned long long*>(my + kFin), 1ull);
+      if (f == gridDim.y - 1) {  // every slice done: every block has read ctr
+        my[kFin] = 0;
+        __threadfence();
+        st_rel(my + kCtr, e);
+      }
+    }
+  }
+}
+
+// Wait for epoch ctr from every rank with a non-empty segment, then (pos != null)
+// ext[pos[i]] = recv[i]; with `ack`, the last block acknowledges to the senders.
+__global__ void __launch_bounds__(kT) peer_wait_kernel(const double* __restrict__ recv,
+                                                        const int* __restrict__ pos, long long n,
+                                                        double* __restrict__ ext, int ack,
+                                                        PeerArgs a) {
+  long long* my = chan_of(a, a.me);
+  const long long e = ld_acq(my + kCtr);  // the sender side of this call site bumped it
+  const int h = threadIdx.x;
+  if (h < a.g && h != a.me && a.off[h + 1] > a.off[h])
+    wait_geq(my + kSig + h, e, a.flags[a.me] + kErrWord);
+  __syncthreads();
+  if (pos != nullptr)
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+      ext[pos[i]] = __ldcg(recv + i);  // written by peers: bypass L1
+  if (!ack) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long d =
+        atomicAdd(reinterpret_cast<unsigned long long*>(my + kDone), 1ull);
+    if (d == gridDim.x - 1) {
+      my[kDone] = 0;
+      for (int s = 0; s < a.g; ++s)
+        if (s != a.me && a.off[s + 1] > a.off[s]) st_rel(chan_of(a, s) + kAck + a.me, e);
+    }
+  }
+}
+
+// acknowledgement alone (receive buffer consumed by a later kernel)
+__global__ void peer_ack_kernel(PeerArgs a) {
+  long long* my = chan_of(a, a.me);
+  const long long e = ld_acq(my + kCtr);
+  const int s = threadIdx.x;
+  if (s < a.g && s != a.me && a.off[s + 1] > a.off[s]) st_rel(chan_of(a, s) + kAck + a.me, e);
+}
+
+// All-gather of k doubles per rank into every rank's out (= buf[h], layout [g][k]);
+// with `reduce`, out[0..k) of this rank = sum over ranks in rank order (buf[h] are
+// then g x k slot areas) — identical bits on every rank.  One block.
+__global__ void __launch_bounds__(kT) peer_gather_kernel(const double* __restrict__ in,
+                                                          long long k, double* out, int reduce,
+                                                          PeerArgs a) {
+  long long* my = chan_of(a, a.me);
+  const long long e = ld_acq(my + kCtr) + 1;
+  __shared__ double vin[16];
+  if (reduce && threadIdx.x < k) vin[threadIdx.x] = in[threadIdx.x];
+  __syncthreads();
+  for (int h = 0; h < a.g; ++h) {
+    if (h != a.me) {
+      if (threadIdx.x == 0) wait_geq(my + kAck + h, e - 1, a.flags[a.me] + kErrWord);
+      __syncthreads();
+    }
+    double* dst = a.buf[h] + static_cast<long long>(a.me) * k;
+    for (long long j = threadIdx.x; j < k; j += blockDim.x) dst[j] = reduce ? vin[j] : in[j];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x < a.g && threadIdx.x != a.me) st_rel(chan_of(a, threadIdx.x) + kSig + a.me, e);
+  if (threadIdx.x < a.g && threadIdx.x != a.me)
+    wait_geq(my + kSig + threadIdx.x, e, a.flags[a.me] + kErrWord);
+  __syncthreads();
+  if (reduce) {
+    const double* slots = a.buf[a.me];
+    if (threadIdx.x < k) {
+      double acc = 0.0;
+      for (int h = 0; h < a.g; ++h) acc += __ldcg(slots + h * k + threadIdx.x);
+      out[threadIdx.x] = acc;
+    }
+  }
+  __syncthreads();  // this rank's slots / out read before the acknowledgement
+  if (threadIdx.x < a.g && threadIdx.x != a.me) st_rel(chan_of(a, threadIdx.x) + kAck + a.me, e);
+  if (threadIdx.x == 0) st_rel(my + kCtr, e);
+}
+
+int fill_peer(PeerArgs* a, int g, int me, int chan, int64_t* const* flags) {
+  if (g < 1 || g > kPeerMax || me < 0 || me >= g || chan < 0 || chan >= DDMGNN_PEER_CHANNELS)
+    return kValueError;
+  *a = PeerArgs{};
+  a->g = g;
+  a->me = me;
+  a->chan = chan;
+  for (int h = 0; h < g; ++h) a->flags[h] = reinterpret_cast<long long*>(flags[h]);
+  return 0;
+}
+
+}  // namespace
+}  // namespace ddmgnn
+
+extern "C" int ddmgnn_peer_put(int g, int me, int chan, int64_t* const* flags, const double* src,
+                               const int32_t* idx, const int64_t* send_off, double* const* dst,
+                               const int64_t* dst_off, void* stream) {
+  PeerArgs a;
+  if (fill_peer(&a, g, me, chan, flags)) return kValueError;
+  long long mx = 0;
+  for (int h = 0; h <= g; ++h) a.off[h] = send_off[h];
+  for (int h = 0; h < g; ++h) {
+    a.buf[h] = dst[h];
+    a.doff[h] = dst_off[h];
+    mx = std::max<long long>(mx, send_off[h + 1] - send_off[h]);
+  }
+  const int bx = std::max(1, std::min(64, static_cast<int>((mx + kT - 1) / kT)));
+  peer_put_kernel<<<dim3(bx, g), kT, 0, static_cast<cudaStream_t>(stream)>>>(src, idx, a);
+  return cuda_status(cudaGetLastError());
+}
+
+extern "C" int ddmgnn_peer_wait(int g, int me, int chan, int64_t* const* flags,
+                                const int64_t* recv_off, const double* recv, const int32_t* pos,
+                                double* ext, int ack, void* stream) {
+  PeerArgs a;
+  if (fill_peer(&a, g, me, chan, flags)) return kValueError;
+  for (int h = 0; h <= g; ++h) a.off[h] = recv_off[h];
+  const long long n = recv_off[g];
+  const int nb = pos ? std::max(1, std::min(64, static_cast<int>((n + kT - 1) / kT))) : 1;
+  peer_wait_kernel<<<nb, kT, 0, static_cast<cudaStream_t>(stream)>>>(recv, pos, n, ext, ack, a);
+  return cuda_status(cudaGetLastError());
+}
+
+extern "C" int ddmgnn_peer_ack(int g, int me, int chan, int64_t* const* flags,
+                               const int64_t* recv_off, void* stream) {
+  PeerArgs a;
+  if (fill_peer(&a, g, me, chan, flags)) return kValueError;
+  for (int h = 0; h <= g; ++h) a.off[h] = recv_off[h];
+  peer_ack_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  return cuda_status(cudaGetLastError());
+}
+
+extern "C" int ddmgnn_peer_allgather(int g, int me, int chan, int64_t* const* flags,
+                                     double* const* out, const double* in, int64_t k,
+                                     void* stream) {
+  PeerArgs a;
+  if (fill_peer(&a, g, me, chan, flags) || k < 0) return kValueError;
+  for (int h = 0; h < g; ++h) a.buf[h] = out[h];
+  peer_gather_kernel<<<1, kT, 0, static_cast<cudaStream_t>(stream)>>>(in, k, nullptr, 0, a);
+  return cuda_status(cudaGetLastError());
+}
+
+extern "C" int ddmgnn_peer_allreduce(int g, int me, int chan, int64_t* const* flags,
+                                     double* const* slots, double* inout, int k, void* stream) {
+  PeerArgs a;
+  if (fill_peer(&a, g, me, chan, flags) || k < 1 || k > 16) return kValueError;
+  for (int h = 0; h < g; ++h) a.buf[h] = slots[h];
+  peer_gather_kernel<<<1, kT, 0, static_cast<cudaStream_t>(stream)>>>(inout, k, inout, 1, a);
+  return cuda_status(cudaGetLastError());
+}
+
+// Peer-visible device buffers and their CUDA IPC handles (the exchange arenas of
+// paper_2402_08296_b200/sharded.py): cudaMalloc'd directly so that a handle names
+// exactly the buffer; opened with lazy peer access from the calling rank's device.
+extern "C" int ddmgnn_peer_alloc(int device, int64_t bytes, void** ptr) {
+  if (!ptr || bytes < 0) return kValueError;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaMalloc(ptr, std::max<int64_t>(bytes, 8));
+  if (e == cudaSuccess) e = cudaMemset(*ptr, 0, std::max<int64_t>(bytes, 8));
+  return cuda_status(e);
+}
+
+extern "C" int ddmgnn_peer_free(void* ptr) { return cuda_status(cudaFree(ptr)); }
+
+extern "C" int ddmgnn_ipc_get(void* ptr, unsigned char* handle) {
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, ptr);
+  if (e == cudaSuccess) memcpy(handle, &h, sizeof(h));
+  return cuda_status(e);
+}
+
+extern "C" int ddmgnn_ipc_open(int device, const unsigned char* handle, void** ptr) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  return cuda_status(e);
+}
+
+extern "C" int ddmgnn_ipc_close(void* ptr) { return cuda_status(cudaIpcCloseMemHandle(ptr)); }

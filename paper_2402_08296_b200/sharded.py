@@ -42,7 +42,8 @@ from .decomp import Decomposition
 from .dss import DssModel, flat_params
 from .sparse import SolveReport
 
-__all__ = ["group_subdomains", "ShardPlan", "plan_shards", "Comm", "PeerExchange", "ShardedDdmGnn"]
+__all__ = ["group_subdomains", "ShardPlan", "plan_shards", "put_layout", "gather_slots", "Comm",
+           "PeerArena", "ShardedDdmGnn"]
 
 
 # ---------------------------------------------------------------------------- planning
@@ -279,58 +280,166 @@ class Comm:
         return recv
 
 
-class PeerExchange:
-    """One-sided exchange over peer memory: every rank maps the other ranks'
-    receive buffers (CUDA IPC handles, all-gathered once) and its gather kernel
-    writes its segment straight into them — over NVLink between the GPUs of one box
-    (P2P), or within one device when several ranks share a GPU (the tests).  The
-    receive layout is the all-to-all one (segments ordered by source rank), so a
-    plan serves both exchange modes.  Ordering: a barrier before the puts (the
-    peers finished reading the previous contents) and after them (the data landed)."""
+def put_layout(plans: list, me: int) -> dict:
+    """Offsets of rank ``me``'s one-sided puts (PeerArena): per destination h the
+    segment [send_off[h], send_off[h+1]) of its send list lands at dst_off[h] of
+    h's receive buffer — the all-to-all layout, segments ordered by source rank —
+    and its own receive buffer holds source h's segment at [recv_off[h],
+    recv_off[h+1]).  Terms land behind the receiver's own v_own local entries."""
+    g = len(plans)
+    p = plans[me]
 
-    def __init__(self, comm: "Comm", recv_buf, recv_counts, send_counts):
-        import torch
+    def cum(c):
+        return np.concatenate(([0], np.cumsum(c))).astype(np.int64)
+
+    return {
+        "halo_send_off": cum(p.halo_send_counts), "halo_recv_off": cum(p.halo_recv_counts),
+        "halo_dst_off": np.array([sum(plans[h].halo_recv_counts[:me]) for h in range(g)],
+                                 dtype=np.int64),
+        "term_send_off": cum(p.term_send_counts), "term_recv_off": cum(p.term_recv_counts),
+        "term_dst_off": np.array([plans[h].v_own + sum(plans[h].term_recv_counts[:me])
+                                  for h in range(g)], dtype=np.int64),
+    }
+
+
+def gather_slots(plan: ShardPlan) -> tuple:
+    """Positions of (R0 r)_i and s_i of every subdomain i in the all-gathered
+    [rank][2 k_slots] buffer (rank g's row = its own subdomains' r0r, then scale)."""
+    ks = plan.k_slots
+    rank, slot = plan.sub_slot // ks, plan.sub_slot % ks
+    return rank * 2 * ks + slot, rank * 2 * ks + ks + slot
+
+
+# Channels of the device-resident exchanges (one per call site; csrc/shard.cu).
+CH_HALO_P, CH_HALO_R, CH_TERMS, CH_GATHER, CH_PQ, CH_RR, CH_RZ, CH_RZO = range(8)
+_FLAG_WORDS = 256   # DDMGNN_PEER_FLAG_WORDS
+_ERR_WORD = _FLAG_WORDS - 1
+_SLOT = 16          # doubles per rank in an all-reduce staging area
+_N_CHANNELS = 8
+
+
+class PeerArena:
+    """Peer-visible device buffers of one rank plus the mappings of every other
+    rank's (CUDA IPC, opened once; NVLink between the GPUs of one box, the same
+    device when several ranks share a GPU in the tests).  The exchanges on it
+    (csrc/shard.cu ``ddmgnn_peer_*``) are one-sided puts ordered by device-side
+    epochs and acknowledgements in the ranks' flag blocks: no host barrier, so a
+    whole sharded PCG iteration is stream-ordered and can be captured in a CUDA
+    graph.  ``sizes``: buffer name -> number of doubles."""
+
+    def __init__(self, comm: "Comm", device: int, sizes: dict):
+        import ctypes
+
         import torch.distributed as dist
-        from torch.multiprocessing.reductions import reduce_tensor
 
-        self.comm = comm
-        self.send_counts = list(send_counts)
-        me, size = comm.rank, comm.size
-        everyone = [None] * size
-        dist.all_gather_object(everyone, (list(recv_counts), reduce_tensor(recv_buf)),
-                               group=comm.group)
-        self.peers = {}
-        for h, (counts, (fn, args)) in enumerate(everyone):
-            if h == me or self.send_counts[h] == 0:
+        self.lib = lib = _lib.load()
+        self.comm, self.device = comm, int(device)
+        g, me = comm.size, comm.rank
+        if g > _FLAG_MAX_RANKS:
+            raise ValueError(f"peer exchange supports at most {_FLAG_MAX_RANKS} ranks")
+        sizes = {"_flags": _FLAG_WORDS, "_slots": _N_CHANNELS * g * _SLOT, **sizes}
+        offsets, total = {}, 0
+        for name, n in sizes.items():
+            offsets[name] = total
+            total += (max(1, int(n)) + 31) // 32 * 32  # 256-byte aligned
+        base = ctypes.c_void_p()
+        _lib.check(lib.ddmgnn_peer_alloc(self.device, 8 * total, ctypes.byref(base)))
+        self._own = base.value
+        handle = ctypes.create_string_buffer(64)
+        _lib.check(lib.ddmgnn_ipc_get(base, handle))
+        everyone = [None] * g
+        dist.all_gather_object(everyone, (handle.raw, offsets), group=comm.group)
+        self._opened = []
+        bases = []
+        for h, (hnd, _offs) in enumerate(everyone):
+            if h == me:
+                bases.append(self._own)
                 continue
-            buf = fn(*args)  # the peer's receive buffer, mapped into this process
-            self.peers[h] = (buf, int(sum(counts[:me])))
-        self._keep = recv_buf
+            ptr = ctypes.c_void_p()
+            _lib.check(lib.ddmgnn_ipc_open(self.device, hnd, ctypes.byref(ptr)))
+            self._opened.append(ptr.value)
+            bases.append(ptr.value)
+        self.g, self.me = g, me
+        self.offsets = offsets
+        self._arr = {}
+        for name in sizes:
+            self._arr[name] = (ctypes.c_void_p * g)(
+                *[bases[h] + 8 * everyone[h][1][name] for h in range(g)])
+        self.flags = self._arr["_flags"]
+        self._slots = {c: (ctypes.c_void_p * g)(
+            *[self._arr["_slots"][h] + 8 * c * g * _SLOT for h in range(g)])
+            for c in range(_N_CHANNELS)}
 
-    def put(self, lib, src_ptr: int, idx, stream: int):
-        """Send segment h of the gather src[idx] into peer h's receive buffer."""
-        self._sync()
-        off = 0
-        for h, cnt in enumerate(self.send_counts):
-            if cnt and h in self.peers:
-                buf, dst = self.peers[h]
-                _lib.check(lib.ddmgnn_gather(src_ptr, idx.data_ptr() + 4 * off, cnt,
-                                             buf.data_ptr() + 8 * dst, stream))
-            off += cnt
-        self._sync()
+    def ptr(self, name: str) -> int:
+        """This rank's own buffer `name` (device pointer)."""
+        return self._arr[name][self.me]
 
-    def _sync(self):
+    def view(self, name: str, n: int, device):
+        return _view_f64(self.ptr(name), n, device)
+
+    @staticmethod
+    def _i64(x):
+        import ctypes
+
+        a = np.ascontiguousarray(x, dtype=np.int64)
+        return a, a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+
+    def put(self, chan, src_ptr, idx_ptr, send_off, dst_name, dst_off, stream):
+        _so, so = self._i64(send_off)
+        _do, do = self._i64(dst_off)
+        _lib.check(self.lib.ddmgnn_peer_put(self.g, self.me, chan, self.flags, src_ptr, idx_ptr,
+                                            so, self._arr[dst_name], do, stream))
+
+    def wait(self, chan, recv_off, recv_ptr, pos_ptr, ext_ptr, ack, stream):
+        _ro, ro = self._i64(recv_off)
+        _lib.check(self.lib.ddmgnn_peer_wait(self.g, self.me, chan, self.flags, ro, recv_ptr,
+                                             pos_ptr, ext_ptr, int(ack), stream))
+
+    def ack(self, chan, recv_off, stream):
+        _ro, ro = self._i64(recv_off)
+        _lib.check(self.lib.ddmgnn_peer_ack(self.g, self.me, chan, self.flags, ro, stream))
+
+    def allreduce_(self, t, chan, stream):
+        """t (contiguous fp64 device tensor, <= 16 values) = sum over ranks, in place."""
+        _lib.check(self.lib.ddmgnn_peer_allreduce(self.g, self.me, chan, self.flags,
+                                                  self._slots[chan], t.data_ptr(), t.numel(),
+                                                  stream))
+
+    def allgather(self, out_name, in_ptr, k, chan, stream):
+        _lib.check(self.lib.ddmgnn_peer_allgather(self.g, self.me, chan, self.flags,
+                                                  self._arr[out_name], in_ptr, k, stream))
+
+    def timed_out(self) -> bool:
+        """A device-side wait gave up (a peer never arrived); synchronising read."""
         import torch
 
-        torch.cuda.current_stream().synchronize()
-        self.comm.barrier()
+        v = _view_i64(self._own + 8 * _ERR_WORD, 1, torch.device("cuda", self.device))
+        return bool(v.item() != 0)
+
+    def close(self):
+        for p in self._opened:
+            self.lib.ddmgnn_ipc_close(p)
+        self._opened = []
+        if self._own:
+            self.lib.ddmgnn_peer_free(self._own)
+            self._own = 0
+
+
+_FLAG_MAX_RANKS = 8  # DDMGNN_PEER_MAX
 
 
 # ---------------------------------------------------------------------------- rank object
 
 
 class ShardedDdmGnn:
-    """Rank-local part of the sharded preconditioner + PCG."""
+    """Rank-local part of the sharded preconditioner + PCG.
+
+    ``exchange="collective"``: halo / term exchanges and the all-gather / all-reduces
+    through torch.distributed (NCCL on device buffers, gloo host-staged).
+    ``exchange="p2p"``: everything through :class:`PeerArena` — one-sided puts into
+    the peers' receive buffers and flag-ordered all-reduces, all on the solve
+    stream, so ``pcg`` and ``capture_apply`` run from CUDA graphs with the host
+    polling the device status only every few iterations."""
 
     def __init__(self, a: sp.csr_matrix, coords: np.ndarray, dec: Decomposition,
                  model: DssModel, level: str = "two", device: int | None = None, group=None,
@@ -340,6 +449,8 @@ class ShardedDdmGnn:
 
         if level not in ("one", "two"):
             raise ValueError(f"level must be 'one' or 'two', got {level!r}")
+        if exchange not in ("collective", "p2p"):
+            raise ValueError(f"exchange must be 'collective' or 'p2p', got {exchange!r}")
         self.comm = Comm(group)
         a = sp.csr_matrix(a)
         if not a.has_sorted_indices:
@@ -378,12 +489,16 @@ class ShardedDdmGnn:
             return torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64), device=dev)
 
         f64 = dict(dtype=torch.float64, device=dev)
+        g, me = self.comm.size, self.comm.rank
         self.own_pos = it(plan.own_pos)
         self.halo_send_idx, self.halo_recv_pos = it(plan.halo_send_idx), it(plan.halo_recv_pos)
         self.term_send_pos = it(plan.term_send_pos)
         self.tptr, self.tent = it(plan.tptr), it(plan.tent.reshape(-1))
         self.pou_own = ft(plan.pou_own)
-        self.sub_slot = it(plan.sub_slot)
+        # (R0 r)_i and s_i of subdomain i in the all-gathered [rank][2 ks] layout
+        ks = plan.k_slots
+        i_r0r, i_scale = gather_slots(plan)
+        self.idx_r0r, self.idx_scale = it(i_r0r), it(i_scale)
         self.kinv = None
         if level == "two":
             cm = coarse_matrix(a, dec)
@@ -393,12 +508,10 @@ class ShardedDdmGnn:
         self.p_ext = torch.zeros(n_loc, **f64)
         self.q_ext = torch.zeros(n_loc, **f64)
         self.halo_send = torch.zeros(max(1, plan.halo_send_idx.size), **f64)
-        self.halo_recv = torch.zeros(max(1, plan.halo_recv_pos.size), **f64)
         self.term_send = torch.zeros(max(1, plan.term_send_pos.size), **f64)
-        self.zloc_ext = torch.zeros(plan.v_own + sum(plan.term_recv_counts) + 1, **f64)
-        ks = plan.k_slots
+        n_hrecv = int(plan.halo_recv_pos.size)
+        n_zext = plan.v_own + sum(plan.term_recv_counts) + 1
         self.gath_in = torch.zeros(2 * ks, **f64)
-        self.gath_out = torch.zeros(2 * ks * self.comm.size, **f64)
         self.own_slot = it(np.arange(plan.own_subs.size))
         self.r0r_full = torch.zeros(self.k, **f64)
         self.scale_full = torch.zeros(self.k, **f64)
@@ -406,21 +519,50 @@ class ShardedDdmGnn:
         self.work = torch.zeros(1184, **f64)
         self.scal = torch.zeros(4, **f64)
         self._all_owned = [pl.owned for pl in plans]
-        if exchange not in ("collective", "p2p"):
-            raise ValueError(f"exchange must be 'collective' or 'p2p', got {exchange!r}")
         self.exchange = exchange
-        self._p2p_halo = self._p2p_terms = None
-        if exchange == "p2p" and self.comm.size > 1:
-            self._p2p_halo = PeerExchange(self.comm, self.halo_recv, plan.halo_recv_counts,
-                                          plan.halo_send_counts)
-            self._p2p_terms = PeerExchange(self.comm, self.zloc_ext[plan.v_own:],
-                                           plan.term_recv_counts, plan.term_send_counts)
+        self.arena = None
+        lay = put_layout(plans, me)
+        self._halo_send_off, self._halo_recv_off = lay["halo_send_off"], lay["halo_recv_off"]
+        self._term_send_off, self._term_recv_off = lay["term_send_off"], lay["term_recv_off"]
+        self._halo_dst_off, self._term_dst_off = lay["halo_dst_off"], lay["term_dst_off"]
+        if exchange == "p2p" and g > 1:
+            self.arena = PeerArena(self.comm, dev.index, {
+                "halo_p": max(1, n_hrecv), "halo_r": max(1, n_hrecv), "zloc_ext": n_zext,
+                "gath_out": 2 * ks * g})
+            self.halo_recv = {CH_HALO_P: self.arena.view("halo_p", max(1, n_hrecv), dev),
+                              CH_HALO_R: self.arena.view("halo_r", max(1, n_hrecv), dev)}
+            self.zloc_ext = self.arena.view("zloc_ext", n_zext, dev)
+            self.gath_out = self.arena.view("gath_out", 2 * ks * g, dev)
+        else:
+            hr = torch.zeros(max(1, n_hrecv), **f64)
+            self.halo_recv = {CH_HALO_P: hr, CH_HALO_R: hr}
+            self.zloc_ext = torch.zeros(n_zext, **f64)
+            self.gath_out = torch.zeros(2 * ks * g, **f64)
+
+    def close(self):
+        """Release the peer mappings (collective: every rank calls it)."""
+        if self.arena is not None:
+            import torch
+
+            torch.cuda.synchronize(self.device)
+            self.comm.barrier()
+            self.arena.close()
+            self.arena = None
+
+    @property
+    def device_ordered(self) -> bool:
+        """Every exchange of an iteration is stream-ordered on the device (peer
+        arena or a single rank), so it can be captured in a CUDA graph."""
+        return self.arena is not None or self.comm.size == 1
 
     def launches_per_apply(self) -> int:
         """Kernels of libddmgnn_b200 launched by one apply_owned."""
         multi = self.comm.size > 1
         gnn = self.ctx.gnn_launches()
-        return (1 + 2 * multi) + gnn + 4 + (self.kinv is not None) + multi + 1
+        halo = 1 + (3 if self.arena is not None else 2) * multi
+        gather = 2 + (1 if self.arena is not None else 0) * multi + 2
+        terms = (3 if self.arena is not None else 1) * multi
+        return halo + gnn + gather + (self.kinv is not None) + terms + 1
 
     # -- helpers --------------------------------------------------------------------------
     def _stream(self):
@@ -431,7 +573,13 @@ class ShardedDdmGnn:
     def _c(self, status):
         _lib.check(status)
 
-    def _halo(self, own_vec, ext_vec):
+    def _allreduce(self, t, chan):
+        if self.arena is not None:
+            self.arena.allreduce_(t, chan, self._stream())
+        else:
+            self.comm.allreduce_(t)
+
+    def _halo(self, own_vec, ext_vec, chan):
         """ext_vec = local-set copy of the distributed vector own_vec (owned + ghosts)."""
         lib, s, p = self._lib, self._stream(), self.plan
         self._c(lib.ddmgnn_scatter(own_vec.data_ptr(), self.own_pos.data_ptr(), p.n_own,
@@ -439,14 +587,19 @@ class ShardedDdmGnn:
         if self.comm.size == 1:
             return ext_vec
         ns, nr = p.halo_send_idx.size, p.halo_recv_pos.size
-        if self._p2p_halo is not None:
-            self._p2p_halo.put(lib, own_vec.data_ptr(), self.halo_send_idx, s)
-        else:
-            self._c(lib.ddmgnn_gather(own_vec.data_ptr(), self.halo_send_idx.data_ptr(), ns,
-                                      self.halo_send.data_ptr(), s))
-            self.comm.alltoallv(self.halo_recv[:nr], self.halo_send[:ns], p.halo_recv_counts,
-                                p.halo_send_counts)
-        self._c(lib.ddmgnn_scatter(self.halo_recv.data_ptr(), self.halo_recv_pos.data_ptr(), nr,
+        recv = self.halo_recv[chan]
+        if self.arena is not None:
+            self.arena.put(chan, own_vec.data_ptr(), self.halo_send_idx.data_ptr(),
+                           self._halo_send_off, "halo_p" if chan == CH_HALO_P else "halo_r",
+                           self._halo_dst_off, s)
+            self.arena.wait(chan, self._halo_recv_off, recv.data_ptr(),
+                            self.halo_recv_pos.data_ptr(), ext_vec.data_ptr(), 1, s)
+            return ext_vec
+        self._c(lib.ddmgnn_gather(own_vec.data_ptr(), self.halo_send_idx.data_ptr(), ns,
+                                  self.halo_send.data_ptr(), s))
+        self.comm.alltoallv(recv[:nr], self.halo_send[:ns], p.halo_recv_counts,
+                            p.halo_send_counts)
+        self._c(lib.ddmgnn_scatter(recv.data_ptr(), self.halo_recv_pos.data_ptr(), nr,
                                    ext_vec.data_ptr(), self._stream()))
         return ext_vec
 
@@ -462,7 +615,7 @@ class ShardedDdmGnn:
         lib, p = self._lib, self.plan
         if z_own is None:
             z_own = torch.empty_like(r_own)
-        self._halo(r_own, self.r_ext)
+        self._halo(r_own, self.r_ext, CH_HALO_R)
         s = self._stream()
         self.ctx.launch_gnn_only(self.r_ext.data_ptr(), s)
         zloc, scale, r0r = self.ctx.local_outputs()
@@ -471,22 +624,24 @@ class ShardedDdmGnn:
         self._c(lib.ddmgnn_gather(r0r, self.own_slot.data_ptr(), ko, self.gath_in.data_ptr(), s))
         self._c(lib.ddmgnn_gather(scale, self.own_slot.data_ptr(), ko,
                                   self.gath_in[ks:].data_ptr(), s))
-        self.comm.allgather(self.gath_out, self.gath_in)
-        g2 = self.gath_out.view(self.comm.size, 2, ks)
-        r0r_all = g2[:, 0, :].reshape(-1).contiguous()
-        sc_all = g2[:, 1, :].reshape(-1).contiguous()
+        if self.arena is not None:
+            self.arena.allgather("gath_out", self.gath_in.data_ptr(), 2 * ks, CH_GATHER, s)
+        else:
+            self.comm.allgather(self.gath_out, self.gath_in)
         s = self._stream()
-        self._c(lib.ddmgnn_gather(r0r_all.data_ptr(), self.sub_slot.data_ptr(), self.k,
+        self._c(lib.ddmgnn_gather(self.gath_out.data_ptr(), self.idx_r0r.data_ptr(), self.k,
                                   self.r0r_full.data_ptr(), s))
-        self._c(lib.ddmgnn_gather(sc_all.data_ptr(), self.sub_slot.data_ptr(), self.k,
+        self._c(lib.ddmgnn_gather(self.gath_out.data_ptr(), self.idx_scale.data_ptr(), self.k,
                                   self.scale_full.data_ptr(), s))
         if self.kinv is not None:
             self._c(lib.ddmgnn_dense_gemv(self.k, self.kinv.data_ptr(), self.r0r_full.data_ptr(),
                                           self.y.data_ptr(), s))
         # own terms + remote terms (owner glues in ascending subdomain order)
         self.zloc_ext[:p.v_own].copy_(_view_f64(zloc, p.v_own, self.device))
-        if self._p2p_terms is not None:
-            self._p2p_terms.put(lib, zloc, self.term_send_pos, s)
+        if self.arena is not None:
+            self.arena.put(CH_TERMS, zloc, self.term_send_pos.data_ptr(), self._term_send_off,
+                           "zloc_ext", self._term_dst_off, s)
+            self.arena.wait(CH_TERMS, self._term_recv_off, 0, None, None, 0, s)
         elif self.comm.size > 1:
             ns = p.term_send_pos.size
             self._c(lib.ddmgnn_gather(zloc, self.term_send_pos.data_ptr(), ns,
@@ -494,11 +649,27 @@ class ShardedDdmGnn:
             nr = sum(p.term_recv_counts)
             self.comm.alltoallv(self.zloc_ext[p.v_own:p.v_own + nr], self.term_send[:ns],
                                 p.term_recv_counts, p.term_send_counts)
+        s = self._stream()
         self._c(lib.ddmgnn_prolong(p.n_own, int(self.kinv is not None), self.tptr.data_ptr(),
                                    self.tent.data_ptr(), self.pou_own.data_ptr(),
                                    self.y.data_ptr(), self.scale_full.data_ptr(),
-                                   self.zloc_ext.data_ptr(), z_own.data_ptr(), self._stream()))
+                                   self.zloc_ext.data_ptr(), z_own.data_ptr(), s))
+        if self.arena is not None:  # the received terms are consumed: let the senders reuse
+            self.arena.ack(CH_TERMS, self._term_recv_off, s)
         return z_own
+
+    def capture_apply(self, r_own, z_own):
+        """A CUDA graph of ``apply_owned(r_own, z_own)`` (device-ordered exchanges only;
+        replay on the current stream)."""
+        import torch
+
+        if not self.device_ordered:
+            raise RuntimeError("graph capture needs exchange='p2p' (or a single rank)")
+        self.apply_owned(r_own, z_own)  # warm-up outside the capture
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            self.apply_owned(r_own, z_own)
+        return graph
 
     def owned_part(self, x_global):
         import torch
@@ -523,8 +694,51 @@ class ShardedDdmGnn:
         return full
 
     # -- Krylov -----------------------------------------------------------------------------
+    def _iteration(self, u, r, pv, q, z, z_old, st, hist, flexible):
+        """One PCG iteration (sparse.py:106-126) as stream work; the scalars live in
+        st (see ddmgnn_pcg_scalars), the updates are no-ops once the solve stopped."""
+        lib, p = self._lib, self.plan
+        n_own = p.n_own
+        stream = self._stream
+        self._halo(pv, self.p_ext, CH_HALO_P)
+        s = stream()
+        self.ctx.spmv_device(self.p_ext.data_ptr(), self.q_ext.data_ptr(), s)
+        self._c(lib.ddmgnn_gather(self.q_ext.data_ptr(), self.own_pos.data_ptr(), n_own,
+                                  q.data_ptr(), s))
+        self._c(lib.ddmgnn_dot(n_own, pv.data_ptr(), q.data_ptr(), self.work.data_ptr(),
+                               st[1:].data_ptr(), s))
+        self._allreduce(st[1:2], CH_PQ)
+        s = stream()
+        self._c(lib.ddmgnn_pcg_scalars(0, st.data_ptr(), hist.data_ptr(), s))
+        self._c(lib.ddmgnn_axpy2_dev(n_own, st.data_ptr(), pv.data_ptr(), q.data_ptr(),
+                                     u.data_ptr(), r.data_ptr(), self.work.data_ptr(),
+                                     st[3:].data_ptr(), s))
+        self._allreduce(st[3:4], CH_RR)
+        self._c(lib.ddmgnn_pcg_scalars(1, st.data_ptr(), hist.data_ptr(), stream()))
+        if flexible:
+            z_old.copy_(z)
+        self.apply_owned(r, z)
+        self._c(lib.ddmgnn_dot(n_own, r.data_ptr(), z.data_ptr(), self.work.data_ptr(),
+                               st[6:].data_ptr(), stream()))
+        if flexible:
+            self._c(lib.ddmgnn_dot_diff(n_own, r.data_ptr(), z.data_ptr(), z_old.data_ptr(),
+                                        self.work.data_ptr(), st[11:].data_ptr(), stream()))
+            self._allreduce(st[11:12], CH_RZO)
+        self._allreduce(st[6:7], CH_RZ)
+        s = stream()
+        self._c(lib.ddmgnn_pcg_scalars(3 if flexible else 2, st.data_ptr(), hist.data_ptr(), s))
+        self._c(lib.ddmgnn_xpby_dev(n_own, z.data_ptr(), st.data_ptr(), pv.data_ptr(), s))
+
+    def _poll(self, st) -> float:
+        """Status of the solve (synchronises): the GNN status word of the applies
+        since the last poll, a timed-out peer wait, then the recurrence's own word."""
+        self.ctx.apply_status(self._stream())  # non-finite model output -> reference error
+        if self.arena is not None and self.arena.timed_out():
+            raise RuntimeError("peer exchange timed out (a rank stopped responding)")
+        return float(st[9].item())
+
     def pcg(self, b_global, tol: float, max_iter: int, check_every: int = 8,
-            flexible: bool = False):
+            flexible: bool = False, graph: bool | None = None):
         """Distributed PCG (sparse.py:76-127) with this preconditioner; collective.
         Returns (u_global, SolveReport) on every rank.  ``flexible=True``: the opt-in
         flexible CG (beta = <r, z - z_old> / rho), as ``sparse.pcg``.
@@ -533,7 +747,9 @@ class ShardedDdmGnn:
         <p, Ap>, ||r||^2 and <r, z> are reduced into it in place by the all-reduces,
         alpha / beta / the stopping test are computed there, and the updates turn into
         no-ops once the solve has stopped — so the host only polls the status every
-        ``check_every`` iterations instead of synchronising on every dot product."""
+        ``check_every`` iterations.  With device-ordered exchanges (``graph`` default)
+        the iteration is captured once in a CUDA graph and replayed; the host issues
+        nothing else between polls."""
         import torch
 
         if tol <= 0:
@@ -541,15 +757,27 @@ class ShardedDdmGnn:
         b = np.asarray(b_global, dtype=np.float64)
         if b.shape != (self.n,):
             raise ValueError(f"expected vector of length {self.n}, got shape {b.shape}")
+        if graph is None:
+            graph = self.device_ordered
         lib, p = self._lib, self.plan
         n_own = p.n_own
-        bo = self.owned_part(b)
-        u = torch.zeros_like(bo)
-        r = bo.clone()
-        q = torch.empty_like(bo)
         max_iter = max(0, int(max_iter))  # sparse.py:105: no iteration for max_iter < 0
-        st = torch.zeros(12, dtype=torch.float64, device=self.device)
-        hist = torch.zeros(max_iter + 1, dtype=torch.float64, device=self.device)
+        # solve buffers persist across calls, so a captured iteration is reused
+        sb = getattr(self, "_solve", None)
+        if sb is None or sb["hist"].numel() < max_iter + 1:
+            f64 = dict(dtype=torch.float64, device=self.device)
+            sb = self._solve = {
+                "u": torch.zeros(n_own, **f64), "r": torch.zeros(n_own, **f64),
+                "q": torch.zeros(n_own, **f64), "z": torch.zeros(n_own, **f64),
+                "pv": torch.zeros(n_own, **f64), "z_old": torch.zeros(n_own, **f64),
+                "st": torch.zeros(12, **f64),
+                "hist": torch.zeros(max(max_iter + 1, 1024), **f64), "graphs": {}}
+        u, r, q, z, pv, st, hist = (sb[k] for k in ("u", "r", "q", "z", "pv", "st", "hist"))
+        bo = self.owned_part(b)
+        u.zero_()
+        r.copy_(bo)
+        st.zero_()
+        hist.zero_()
         stream = self._stream
         self._dot(bo, bo, 0)
         nb = float(np.sqrt(self._allreduce_scalar(0)))
@@ -558,52 +786,37 @@ class ShardedDdmGnn:
         # r0 = b, so history[0] = ||b|| / ||b|| = 1 exactly (sparse.py:96-99)
         if 1.0 < tol:
             return np.zeros(self.n), SolveReport(0, [1.0], True, 1.0, tol)
-        z = self.apply_owned(r)
+        self.apply_owned(r, z)
         self.ctx.apply_status(self._stream())  # non-finite model output -> reference error
-        pv = z.clone()
-        z_old = torch.empty_like(z) if flexible else None
+        pv.copy_(z)
+        z_old = sb["z_old"] if flexible else None
         self._c(lib.ddmgnn_dot(n_own, r.data_ptr(), z.data_ptr(), self.work.data_ptr(),
                                st[0:].data_ptr(), stream()))
-        self.comm.allreduce_(st[0:1])  # rho = <r0, z0>
+        self._allreduce(st[0:1], CH_RZ)  # rho = <r0, z0>
         st[4], st[5], st[10] = nb, float(tol), float(max_iter)
         hist[0] = 1.0  # r0 = b
-        status = 0.0
-        for it in range(max_iter):
-            self._halo(pv, self.p_ext)
-            s = stream()
-            self.ctx.spmv_device(self.p_ext.data_ptr(), self.q_ext.data_ptr(), s)
-            self._c(lib.ddmgnn_gather(self.q_ext.data_ptr(), self.own_pos.data_ptr(), n_own,
-                                      q.data_ptr(), s))
-            self._c(lib.ddmgnn_dot(n_own, pv.data_ptr(), q.data_ptr(), self.work.data_ptr(),
-                                   st[1:].data_ptr(), s))
-            self.comm.allreduce_(st[1:2])
-            s = stream()
-            self._c(lib.ddmgnn_pcg_scalars(0, st.data_ptr(), hist.data_ptr(), s))
-            self._c(lib.ddmgnn_axpy2_dev(n_own, st.data_ptr(), pv.data_ptr(), q.data_ptr(),
-                                         u.data_ptr(), r.data_ptr(), self.work.data_ptr(),
-                                         st[3:].data_ptr(), s))
-            self.comm.allreduce_(st[3:4])
-            self._c(lib.ddmgnn_pcg_scalars(1, st.data_ptr(), hist.data_ptr(), stream()))
-            if (it + 1) % check_every == 0 or it + 1 == max_iter:
-                # the GNN status word of the applies since the last check, then the
-                # solve's own status (both are device-side words: one poll each)
-                self.ctx.apply_status(stream())
-                status = float(st[9].item())
-                if status != 0.0:
+        args = (u, r, pv, q, z, z_old, st, hist, flexible)
+        it = 0
+        if max_iter > 0:
+            # the first iteration runs eagerly (warms every kernel / communicator up)
+            self._iteration(*args)
+            it = 1
+        gx = None
+        if graph and it < max_iter and self._poll(st) == 0.0:
+            gx = sb["graphs"].get(flexible)
+            if gx is None:
+                gx = sb["graphs"][flexible] = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gx):
+                    self._iteration(*args)
+        while it < max_iter:
+            if gx is not None:
+                gx.replay()
+            else:
+                self._iteration(*args)
+            it += 1
+            if it % check_every == 0 or it == max_iter:
+                if self._poll(st) != 0.0:
                     break
-            if flexible:
-                z_old.copy_(z)
-            self.apply_owned(r, z)
-            self._c(lib.ddmgnn_dot(n_own, r.data_ptr(), z.data_ptr(), self.work.data_ptr(),
-                                   st[6:].data_ptr(), stream()))
-            if flexible:
-                self._c(lib.ddmgnn_dot_diff(n_own, r.data_ptr(), z.data_ptr(), z_old.data_ptr(),
-                                            self.work.data_ptr(), st[11:].data_ptr(), stream()))
-                self.comm.allreduce_(st[11:12])
-            self.comm.allreduce_(st[6:7])
-            s = stream()
-            self._c(lib.ddmgnn_pcg_scalars(3 if flexible else 2, st.data_ptr(), hist.data_ptr(), s))
-            self._c(lib.ddmgnn_xpby_dev(n_own, z.data_ptr(), st.data_ptr(), pv.data_ptr(), s))
         sh = st.cpu().numpy()
         status, iters = int(sh[9]), int(sh[8])
         if status == 3:
@@ -615,7 +828,7 @@ class ShardedDdmGnn:
 
     def _allreduce_scalar(self, slot: int) -> float:
         t = self.scal[slot:slot + 1]
-        self.comm.allreduce_(t)
+        self._allreduce(t, CH_PQ)
         return float(t.item())
 
 
@@ -628,6 +841,16 @@ def _view_f64(ptr: int, n: int, device):
 
     class _Cai:
         __cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False),
+                                    "version": 3, "strides": None}
+
+    return torch.as_tensor(_Cai(), device=device)
+
+
+def _view_i64(ptr: int, n: int, device):
+    import torch
+
+    class _Cai:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<i8", "data": (ptr, False),
                                     "version": 3, "strides": None}
 
     return torch.as_tensor(_Cai(), device=device)

@@ -3,7 +3,11 @@ share cuda:0 and talk through gloo (host-staged collectives); the kernels are
 the same ones the NCCL path runs.  Checks: the sharded apply equals the
 single-GPU apply bit for bit (the owner glues terms in the reference's order,
 hybrid.py:133-135), and the distributed PCG (sparse.py:76-127) converges in the
-reference's iteration count (+-1) on config A with the pinned desk weights."""
+reference's iteration count (+-1) on config A with the pinned desk weights.  With
+exchange="p2p" every exchange is a device-flag-ordered put over CUDA-IPC peer
+memory (csrc/shard.cu ddmgnn_peer_*): the apply and the PCG iteration are replayed
+from CUDA graphs with no host barrier (on one shared GPU the ranks' spinning waits
+make progress through context time-slicing)."""
 import os
 import socket
 
@@ -48,8 +52,23 @@ def _worker(rank, world, port, q):
                 key = f"apply_{level}_maxdiff" + ("" if exch == "collective" else "_p2p")
                 out[key] = float(np.max(np.abs(z - z_ref)))
         sh = ShardedDdmGnn(a, coords, dec, model, level="two", exchange="p2p")
-        u, rep = sh.pcg(b, 1e-6, 500)
+        # the device-ordered apply replayed from a CUDA graph: same bits
+        r_own = sh.owned_part(g["r"])
+        z_own = torch.empty_like(r_own)
+        gx = sh.capture_apply(r_own, z_own)
+        for _ in range(3):
+            gx.replay()
+        torch.cuda.synchronize()
+        z_ref2 = ddm.build_ddm_gnn(a, coords, dec, model, level="two")(g["r"])
+        out["apply_graph_maxdiff"] = float(np.max(np.abs(sh.gather_global(z_own) - z_ref2)))
+        u, rep = sh.pcg(b, 1e-6, 500)  # graph-replayed iterations, device flags only
         out["p2p_iters"] = rep.iterations
+        out["p2p_relres"] = float(np.linalg.norm(b - a @ u) / np.linalg.norm(b))
+        u, rep = sh.pcg(b, 1e-6, 500, graph=False)
+        out["p2p_eager_iters"] = rep.iterations
+        u, rep = sh.pcg(b, 1e-6, 500, flexible=True)
+        out["p2p_fcg_iters"] = rep.iterations
+        sh.close()
         sh = ShardedDdmGnn(a, coords, dec, model, level="two")
         u, rep = sh.pcg(b, 1e-6, 500)
         res = np.linalg.norm(b - a @ u) / np.linalg.norm(b)
@@ -84,6 +103,10 @@ def test_sharded_apply_and_pcg_match_single_gpu(world):
         assert out["apply_one_maxdiff"] == 0.0, out
         assert out["apply_two_maxdiff_p2p"] == 0.0 and out["apply_one_maxdiff_p2p"] == 0.0, out
         assert abs(out["p2p_iters"] - ref_iters) <= 1, out
+        assert out["p2p_eager_iters"] == out["p2p_iters"], out
+        assert out["p2p_relres"] < 1.01e-6, out
+        assert out["apply_graph_maxdiff"] == 0.0, out
+        assert out["p2p_fcg_iters"] <= out["p2p_iters"] + 1, out
         assert out["converged"] and abs(out["iters"] - ref_iters) <= 1, (out, ref_iters)
         assert out["relres"] < 1.01e-6
         assert out["hist_len"] == out["iters"] + 1

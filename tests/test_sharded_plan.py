@@ -57,6 +57,54 @@ def test_plans_partition_dofs_and_cover_terms(n_ranks):
         assert p.pou_own.shape == p.owned.shape
 
 
+@pytest.mark.parametrize("n_ranks", [2, 3, 5])
+def test_one_sided_put_layout_routes_every_value(n_ranks):
+    """The peer-memory puts (PeerArena, sharded.put_layout) simulated on host
+    arrays: every ghost of every rank receives its owner's value, every remote
+    prolongation term lands where the owner's transpose map reads it, and the
+    all-gather slots name each subdomain's (R0 r)_i / s_i."""
+    from paper_2402_08296_b200.sharded import gather_slots, plan_shards, put_layout
+
+    a, _b, coords, dec = _problem()
+    plans = plan_shards(a, coords, dec, n_ranks)
+    x = np.random.default_rng(0).standard_normal(dec.n_dofs)
+    lays = [put_layout(plans, g) for g in range(n_ranks)]
+    halo_recv = [np.full(max(1, p.halo_recv_pos.size), np.nan) for p in plans]
+    zloc_ext = [np.full(p.v_own + sum(p.term_recv_counts) + 1, np.nan) for p in plans]
+    # batched local values: subdomain i's entry k gets 1000 * i + k
+    zloc = []
+    for p in plans:
+        zloc.append(np.concatenate([1000.0 * i + np.arange(dec.subdomains[i].size)
+                                    for i in p.own_subs]) if p.own_subs.size else np.zeros(0))
+    for me, p in enumerate(plans):
+        lay = lays[me]
+        x_own = x[p.owned]
+        for h in range(n_ranks):
+            b0, b1 = lay["halo_send_off"][h], lay["halo_send_off"][h + 1]
+            d0 = lay["halo_dst_off"][h]
+            halo_recv[h][d0:d0 + b1 - b0] = x_own[p.halo_send_idx[b0:b1]]
+            t0, t1 = lay["term_send_off"][h], lay["term_send_off"][h + 1]
+            e0 = lay["term_dst_off"][h]
+            zloc_ext[h][e0:e0 + t1 - t0] = zloc[me][p.term_send_pos[t0:t1]]
+    for g, p in enumerate(plans):
+        ext = np.full(p.n_loc, np.nan)
+        ext[p.own_pos] = x[p.owned]
+        ext[p.halo_recv_pos] = halo_recv[g][:p.halo_recv_pos.size]
+        assert np.array_equal(ext, x[p.local])
+        zloc_ext[g][:p.v_own] = zloc[g]
+        for t, j in enumerate(p.owned):
+            for pos, i in p.tent[p.tptr[t]:p.tptr[t + 1]]:
+                k = int(np.searchsorted(dec.subdomains[i], j))
+                assert zloc_ext[g][pos] == 1000.0 * i + k
+        i_r0r, i_sc = gather_slots(p)
+        ks = p.k_slots
+        for i in range(dec.n_subdomains):
+            owner = int(i_r0r[i] // (2 * ks))
+            assert i in plans[owner].own_subs
+            row = int(np.flatnonzero(plans[owner].own_subs == i)[0])
+            assert i_r0r[i] == owner * 2 * ks + row and i_sc[i] == i_r0r[i] + ks
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
