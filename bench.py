@@ -73,15 +73,33 @@ def gnn_flops(k_bar, d, v, e):
     return float(k_bar * (per_node * v + 16 * d * e) + (2 * d * d + 2 * d) * v)
 
 
-def gnn_flops_exec(k_bar, d, v, e):
+def gnn_flops_exec(k_bar, d, v, e, h0_skip=False):
     """FP32 flops the fused kernel executes (FMA = 2, relu not counted):
     per node and layer Q and P ((d+2) -> 2d each), psi first layer ((3d+2) -> d with the
     messages' second layer folded in), psi second layer (d -> d), h update (d);
-    per edge and layer P+Q add, |d| FMA, sum add over 2d hidden units; decoder once."""
+    per edge and layer P+Q add, |d| FMA, sum add over 2d hidden units; decoder once.
+    With h0_skip the first layer skips the h rows of P, Q and psi (h = 0)."""
     dh = (d + 1) // 2 * 2
     per_node = 2 * (2 * (d + 2) * 2 * d) + 2 * (3 * d + 2) * dh + 2 * d * dh + 2 * dh
     per_edge = 2 * d * (1 + 2 + 1)
-    return float(k_bar * (per_node * v + per_edge * e) + (2 * d * dh + 2 * d) * v)
+    skipped = (2 * (2 * d * 2 * d) + 2 * d * dh) * v if h0_skip else 0
+    return float(k_bar * (per_node * v + per_edge * e) + (2 * d * dh + 2 * d) * v - skipped)
+
+
+def fp32_peak_tflops(sm_mhz):
+    """FP32 CUDA-core peak: the FFMA2 microbenchmark measured on this pool's B200s
+    (profiles/r02_fp32_peak.json, tools/ubench/fp32_peak.cu, with its clock record),
+    else the nominal 148 SM x 128 lanes x 2 flop x sm_max_mhz."""
+    nominal = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+    try:
+        rec = json.load(open(os.path.join(ROOT, "profiles", "r02_fp32_peak.json")))
+        return float(rec["fp32_ffma2_tflops"]), (
+            f"measured FFMA2 peak {rec['fp32_ffma2_tflops']:.1f} TFLOP/s at "
+            f"{rec.get('sm_mhz_median', '?')} MHz (profiles/r02_fp32_peak.json, "
+            f"tools/ubench/fp32_peak.cu); nominal {nominal:.1f} at {sm_mhz:.0f} MHz")
+    except (OSError, ValueError, KeyError):
+        return nominal, ("nominal 148 SM x 128 FP32 lanes x 2 flop x sm_max_mhz (no measured "
+                         "FP32 figure committed)")
 
 
 def profiled_traffic(kernel):
@@ -587,10 +605,13 @@ def run_ours(args):
     hbm_src = "MEASURED_PEAKS.json (of measured)" if "hbm_gbs" in peaks else \
         "fallback 6.65 TB/s from B200_PROFILING.md (of fallback; MEASURED_PEAKS.json absent)"
     sm_mhz = peaks.get("sm_max_mhz") or clk.summary().get("sm_max_mhz") or 1965.0
-    fp32_peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
-    flops = gnn_flops_exec(info["k_bar"], info["d"], info["V"], info["E"])
+    fp32_peak, fp32_src = fp32_peak_tflops(sm_mhz)
+    h0 = os.environ.get("DDMGNN_H0_SKIP", "1") != "0"
+    flops_exec = gnn_flops_exec(info["k_bar"], info["d"], info["V"], info["E"], h0)
     flops_survey = gnn_flops(info["k_bar"], info["d"], info["V"], info["E"])
-    achieved = flops / (gnn_ms * 1e-3) / 1e12
+    # the contract's algorithmic figure: SURVEY.md §8(d)'s F_gnn per launch
+    achieved = flops_survey / (gnn_ms * 1e-3) / 1e12
+    achieved_exec = flops_exec / (gnn_ms * 1e-3) / 1e12
     gnn_traffic, traffic_src = profiled_traffic("gnn_kernel")
     spmv_traffic, _ = profiled_traffic("spmv_kernel")
     # per chunk: gnn_kernel, one launch per cluster size, and for subdomains beyond an
@@ -613,12 +634,15 @@ def run_ours(args):
                 "bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
                 "frac": achieved / fp32_peak, "traffic": gnn_traffic,
                 "traffic_source": traffic_src,
-                "algorithmic": f"executed FP32 flops k(1820 V + 80 E) + 220 V (d=10) = {flops:.3e} "
-                               "per launch (DESIGN.md §4)",
-                "survey_F_gnn": flops_survey,
-                "survey_F_gnn_tflops": flops_survey / (gnn_ms * 1e-3) / 1e12,
-                "peak_source": "148 SM x 128 FP32 lanes x 2 flop x sm_max_mhz (FP32 CUDA-core "
-                               "peak; MEASURED_PEAKS has no FP32 figure)",
+                "algorithmic": f"SURVEY.md §8(d) F_gnn = k(2120 V + 160 E) + 220 V (d=10) = "
+                               f"{flops_survey:.3e} per launch (V={info['V']}, E={info['E']})",
+                "executed_flops": flops_exec,
+                "executed_tflops": achieved_exec,
+                "frac_executed": achieved_exec / fp32_peak,
+                "executed_note": "FP32 flops the kernel actually issues: k(1820 V + 80 E) + 220 V"
+                                 + (" - 1000 V (layer 1 on h = 0)" if h0 else "")
+                                 + " at d=10 (FMA = 2, relu not counted; DESIGN.md §4)",
+                "peak_source": fp32_src,
                 "gnn_ms": gnn_ms, "share_of_step": gnn_ms / ms,
             },
             "roofline_spmv": {
