@@ -77,6 +77,18 @@ struct ddmgnn_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // big-subdomain GNN kernel (forked from the apply stream)
+  // staged input of ddmgnn_apply_host: r copied in kStages chunks on `copy`, each
+  // followed by a stream write of its ready flag; the GNN CTAs (subdomains ordered by
+  // the last chunk they read) start as soon as their chunk has landed
+  cudaStream_t copy = nullptr;
+  cudaEvent_t ev_copied = nullptr;
+  unsigned int* d_ready = nullptr;  // kStages flags
+  int* d_sub_stage = nullptr;       // per subdomain: index of the last chunk it reads
+  int* d_order_staged = nullptr;    // big subdomains first (as order), then by stage, LPT
+  int staged_ok = 0;                // no flat-path subdomains and stream memory ops work
+  int stage_now = 0;                // set while apply_host enqueues a staged apply
+  unsigned int stage_epoch = 0;
+  long long stage_chunk = 0;        // doubles per chunk (multiple of 16: 128-byte lines)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // matrix
   int n = 0;
@@ -167,6 +179,8 @@ extern "C" int ddmgnn_create(int device, ddmgnn_ctx** out) {
     return fail(kCudaError, cudaGetErrorString(e));
   }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_copied, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
   if (e != cudaSuccess) {
@@ -197,6 +211,8 @@ static void free_layout(ddmgnn_ctx* c) {
   dfree(c->d_r0r); dfree(c->d_scale); dfree(c->d_zloc); dfree(c->d_y);
   dfree(c->d_bad); dfree(c->d_outbad);
   dfree(c->d_hbuf); dfree(c->d_cbuf); dfree(c->d_qbuf); dfree(c->d_bslices); dfree(c->d_csubs);
+  dfree(c->d_sub_stage); dfree(c->d_order_staged);
+  c->staged_ok = 0;
   dfree(c->d_ainv); dfree(c->d_ainv_off);
   c->have_asm = false;
   c->n_bslices = 0;
@@ -215,7 +231,7 @@ extern "C" void ddmgnn_destroy(ddmgnn_ctx* c) {
   dfree(c->d_ic_state);
   dfree(c->d_sell_off); dfree(c->d_sell_col); dfree(c->d_sell_val);
   dfree(c->d_bank); dfree(c->d_cinv); dfree(c->d_status);
-  dfree(c->d_rin); dfree(c->d_zout);
+  dfree(c->d_rin); dfree(c->d_zout); dfree(c->d_ready);
   dfree(c->d_b); dfree(c->d_u); dfree(c->d_r); dfree(c->d_p); dfree(c->d_q); dfree(c->d_z);
   dfree(c->d_partials); dfree(c->d_hist); dfree(c->d_st); dfree(c->d_zold);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -225,6 +241,8 @@ extern "C" void ddmgnn_destroy(ddmgnn_ctx* c) {
   if (c->side) cudaStreamDestroy(c->side);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->copy) cudaStreamDestroy(c->copy);
+  if (c->ev_copied) cudaEventDestroy(c->ev_copied);
   delete c;
 }
 
@@ -384,6 +402,64 @@ extern "C" int ddmgnn_set_coarse_inverse(ddmgnn_ctx* c, int64_t k, const double*
 }
 
 
+// ---- staged input of ddmgnn_apply_host -------------------------------------------
+constexpr int kStages = 4;
+
+// cuStreamWriteValue32 (driver API, resolved at run time so the library has no
+// link-time dependency on libcuda): the copy stream writes a chunk's ready flag
+// once the chunk's H2D copy has completed, with a memory barrier before the write.
+using WriteValue32Fn = int (*)(cudaStream_t, unsigned long long, unsigned int, unsigned int);
+static WriteValue32Fn write_value32() {
+  static WriteValue32Fn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<WriteValue32Fn>(p);
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+
+// Chunk c of r = DOFs [c chunk, (c+1) chunk); subdomain i reads up to its largest
+// DOF, so it may start after chunk max_i / chunk.  Order for the staged launch: the
+// n_big leading (cluster-path) subdomains as in the LPT order, then the rest by
+// stage, LPT within a stage (stable partition of the LPT order).
+static cudaError_t plan_staged_input(ddmgnn_ctx* c, int n_big, bool has_flat) {
+  dfree(c->d_sub_stage);
+  dfree(c->d_order_staged);
+  c->staged_ok = 0;
+  const char* env = getenv("DDMGNN_STAGED_INPUT");
+  if ((env && env[0] == '0') || has_flat || c->n <= 0 || c->K <= 0) return cudaSuccess;
+  const long long chunk = ((static_cast<long long>(c->n) + kStages - 1) / kStages + 15) / 16 * 16;
+  std::vector<int> stage(c->K);
+  for (int i = 0; i < c->K; ++i) {
+    int64_t mx = 0;
+    for (int64_t t = c->sub_ptr[i]; t < c->sub_ptr[i + 1]; ++t) mx = std::max(mx, c->sub_idx[t]);
+    stage[i] = static_cast<int>(std::min<long long>(kStages - 1, mx / chunk));
+  }
+  const auto& ord = c->lay.h_order;
+  std::vector<int> staged(ord.begin(), ord.begin() + n_big);
+  for (int st = 0; st < kStages; ++st)
+    for (int t = n_big; t < c->K; ++t)
+      if (stage[ord[t]] == st) staged.push_back(ord[t]);
+  cudaError_t e = upload(&c->d_sub_stage, stage);
+  if (e == cudaSuccess) e = upload(&c->d_order_staged, staged);
+  if (e == cudaSuccess && !c->d_ready) {
+    e = cudaMalloc(&c->d_ready, sizeof(unsigned int) * kStages);
+    if (e == cudaSuccess) e = cudaMemset(c->d_ready, 0, sizeof(unsigned int) * kStages);
+    c->stage_epoch = 0;
+  }
+  if (e != cudaSuccess) return e;
+  c->stage_chunk = chunk;
+  c->staged_ok = write_value32() != nullptr;
+  return cudaSuccess;
+}
+
 // Plan the shared-memory placement for the current latent dimension and
 // (re)allocate the per-node global scratch it needs.
 static int refresh_classes(ddmgnn_ctx* c) {
@@ -463,6 +539,7 @@ static int refresh_classes(ddmgnn_ctx* c) {
   CUDA_TRY(dalloc(&c->d_hbuf, (multi || nb) ? (V + c->K) * hs : 0));
   CUDA_TRY(dalloc(&c->d_cbuf, (multi || nb) ? V : 0));
   CUDA_TRY(dalloc(&c->d_qbuf, bsl.empty() ? 0 : (V + c->K) * qs));
+  CUDA_TRY(plan_staged_input(c, nb, !bsl.empty()));
   dfree(c->d_bslices);
   c->n_bslices = static_cast<int>(bsl.size());
   while (bsl.size() % kFlatWarps) bsl.push_back(make_int2(-1, 0));  // padding slices
@@ -679,6 +756,17 @@ static cudaError_t enqueue_gnn_impl(ddmgnn_ctx* c, const double* r, int* status,
     if (e != cudaSuccess) return e;
     a.first = ch == 0;
     a.last = ch == nch - 1;
+    if (c->stage_now && ch == 0) {  // ddmgnn_apply_host: r still arriving in chunks
+      a.order = c->d_order_staged;
+      a.ready = c->d_ready;
+      a.sub_stage = c->d_sub_stage;
+      a.epoch = c->stage_epoch;
+    } else {
+      a.order = L.order;
+      a.ready = nullptr;
+      a.sub_stage = nullptr;
+      a.epoch = 0;
+    }
     a.layer0 = ch * M.lmax + 1;
     a.nl = std::min(M.lmax, M.k_bar - ch * M.lmax);
     a.order_begin = 0;
@@ -815,9 +903,34 @@ extern "C" int ddmgnn_apply_host(ddmgnn_ctx* c, const double* r, double* z, int 
     std::memcpy(c->h_pin_a, r, bytes);
     src = c->h_pin_a;
   }
-  CUDA_TRY(cudaMemcpyAsync(c->d_rin, src, bytes, cudaMemcpyHostToDevice, s));
-  CUDA_TRY(cudaMemsetAsync(c->d_status, 0, sizeof(int), s));
-  CUDA_TRY(enqueue_apply(c, c->d_rin, c->d_zout, level, c->d_status, nullptr, 0, s));
+  const bool gnn = level == DDMGNN_LEVEL_ONE || level == DDMGNN_LEVEL_TWO;
+  if (gnn && c->staged_ok) {
+    // r in kStages chunks on the copy stream, each followed by its ready flag; the
+    // GNN's CTAs (ordered by the chunk they need) start on the first chunk while the
+    // rest is still crossing PCIe
+    const unsigned int ep = ++c->stage_epoch;
+    WriteValue32Fn wv = write_value32();
+    for (int ci = 0; ci < kStages; ++ci) {
+      const long long off = ci * c->stage_chunk;
+      const long long cnt = std::min<long long>(c->stage_chunk, c->n - off);
+      if (cnt > 0)
+        CUDA_TRY(cudaMemcpyAsync(c->d_rin + off, src + off, sizeof(double) * cnt,
+                                 cudaMemcpyHostToDevice, c->copy));
+      if (wv(c->copy, reinterpret_cast<unsigned long long>(c->d_ready + ci), ep, 0) != 0)
+        return fail(kCudaError, "cuStreamWriteValue32 failed");
+    }
+    CUDA_TRY(cudaEventRecord(c->ev_copied, c->copy));
+    CUDA_TRY(cudaMemsetAsync(c->d_status, 0, sizeof(int), s));
+    c->stage_now = 1;
+    cudaError_t e = enqueue_apply(c, c->d_rin, c->d_zout, level, c->d_status, nullptr, 0, s);
+    c->stage_now = 0;
+    CUDA_TRY(e);
+    CUDA_TRY(cudaStreamWaitEvent(s, c->ev_copied, 0));  // formal join of the copy stream
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(c->d_rin, src, bytes, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemsetAsync(c->d_status, 0, sizeof(int), s));
+    CUDA_TRY(enqueue_apply(c, c->d_rin, c->d_zout, level, c->d_status, nullptr, 0, s));
+  }
   CUDA_TRY(cudaMemcpyAsync(z_pin ? z : c->h_pin_b, c->d_zout, bytes, cudaMemcpyDeviceToHost, s));
   st = check_status_word(c, s);
   if (st) return st;

@@ -156,6 +156,11 @@ struct GnnArgs {
   int cluster_count[3];  // subdomains per cluster size 2, 4, 8 (csubs laid out in that order)
   int cluster_smem[3];   // dynamic shared memory per CTA of each cluster-size class
   int cluster_threads[3];  // threads per CTA (448 when two CTAs fit an SM, else kGnnThreads)
+  // staged input (ddmgnn_apply_host): r arrives in chunks; subdomain i may start once
+  // ready[sub_stage[i]] >= epoch (flags written by the copy stream).  null = no wait.
+  const unsigned int* ready;
+  const int* sub_stage;
+  unsigned int epoch;
 };
 int gnn_smem_max_nodes(int d);
 // WQ WP B1 WL WU BP1 WP2 BP2 STRIDE D2P DP DEC_W1 DEC_B1 DEC_W2 DEC_B2 LMAX (gnn_cfg.h)

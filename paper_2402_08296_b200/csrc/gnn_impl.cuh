@@ -835,6 +835,22 @@ struct GnnShared {
   uint32_t tmem;
 };
 
+// Staged input: wait until the chunk of r this subdomain reads has arrived (flag
+// written by the copy stream after the chunk's H2D copy; ddmgnn_apply_host).
+__device__ __forceinline__ void wait_input(const GnnArgs& a, int sub) {
+  if (a.ready == nullptr) return;
+  if (threadIdx.x == 0) {
+    const unsigned int* f = a.ready + a.sub_stage[sub];
+    unsigned int v;
+    while (true) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+      if (static_cast<int>(v - a.epoch) >= 0) break;
+      __nanosleep(256);
+    }
+  }
+  __syncthreads();
+}
+
 // Restriction of r to subdomain `sub` (hybrid.py:103-108) and its coarse RHS row
 // (R0 r)_i, by the whole CTA: writes scale/r0r, c (fp32 r_i / s_i) into c_out and
 // zeroes h rows 0..k-1.  Returns s_i (uniform).
@@ -846,7 +862,7 @@ __device__ __forceinline__ double restrict_sub(const GnnArgs& a, GnnShared& sh, 
   double ss = 0.0, rr0 = 0.0;
   for (int n = tid; n < k; n += nthr) {
     const int g = a.idx[pos0 + n];
-    const double v = a.r[g];
+    const double v = __ldcg(a.r + g);  // L2: r may still be arriving in chunks
     ss = fma(v, v, ss);
     rr0 = fma(a.pou[g], v, rr0);
     scratch[n] = v;
@@ -904,6 +920,7 @@ __global__ void __launch_bounds__(gnn_cta_threads<D>(), 1) gnn_kernel(GnnArgs a)
   if (tid == 0) sh.bad = 0;
   double s;
   if (a.first) {
+    wait_input(a, sub);
     s = restrict_sub<D>(a, sh, sub, pos0, k, reinterpret_cast<double*>(ns.q), ns.c, ns.h);
     if (s == 0.0) {
       if (tid == 0) {
@@ -1148,11 +1165,12 @@ __global__ void __launch_bounds__(gnn_cta_threads<D>(), 1) gnn_cluster_kernel(Gn
   }
   double s;
   if (a.first) {
+    wait_input(a, sub);
     double* scratch = reinterpret_cast<double*>(ns.q);
     double ss = 0.0, rr0 = 0.0;
     for (int n = tid; n < cnt; n += nthr) {
       const int g = a.idx[pos0 + lo + n];
-      const double v = a.r[g];
+      const double v = __ldcg(a.r + g);
       ss = fma(v, v, ss);
       rr0 = fma(a.pou[g], v, rr0);
       scratch[n] = v;

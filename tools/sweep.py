@@ -2,7 +2,8 @@
 message-passing depth on synthetic blob meshes (target >= 50 N_s nodes so K >= 50),
 random-init weights, d = 10 (or --dims).  One JSON line per configuration:
 applies timed with CUDA events (L2 flushed), executed FP32 TFLOP/s of the GNN
-launch against the FP32 CUDA-core peak (bench.py's roofline definition).
+launch against the measured FP32 peak (bench.py's roofline definitions: executed flops
+and SURVEY §8(d)'s F_gnn).
 
     python tools/sweep.py [--sizes 500,1000,2000,5000] [--overlaps 1,2,3] [--kbars 5,10,20,30]
 """
@@ -18,7 +19,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_2402_08296_b200 as ddm  # noqa: E402
-from bench import gnn_flops_exec  # noqa: E402
+from bench import fp32_peak_tflops, gnn_flops, gnn_flops_exec  # noqa: E402
 from paper_2402_08296_b200.problem import ProblemConfig, build_problem  # noqa: E402
 
 
@@ -35,7 +36,8 @@ def main():
     st = torch.cuda.Stream()
     torch.cuda.set_stream(st)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
-    peak = 148 * 128 * 2 * 1965e6 / 1e12
+    peak, peak_src = fp32_peak_tflops(1965.0)
+    h0 = os.environ.get("DDMGNN_H0_SKIP", "1") != "0"
     for ns in [int(x) for x in args.sizes.split(",")]:
         for ov in [int(x) for x in args.overlaps.split(",")]:
             t0 = time.perf_counter()
@@ -69,13 +71,16 @@ def main():
                         torch.cuda.synchronize()
                         dst.append(e0.elapsed_time(e1))
                 gms = float(np.median(tg))
-                fl = gnn_flops_exec(kb, dd, info["V"], info["E"])
+                fl = gnn_flops_exec(kb, dd, info["V"], info["E"], h0)
+                fs = gnn_flops(kb, dd, info["V"], info["E"])
                 print(json.dumps({
                     "N_s": ns, "overlap": ov, "k_bar": kb, "d": dd, "N": prob.system.n, "K": info["K"],
                     "V": info["V"], "E": info["E"], "k_max": info["k_max"], "n_big": info["n_big"],
                     "apply_ms": float(np.median(ta)), "gnn_ms": gms,
                     "gnn_tflops": fl / (gms * 1e-3) / 1e12,
                     "frac_fp32": fl / (gms * 1e-3) / 1e12 / peak,
+                    "F_gnn_tflops": fs / (gms * 1e-3) / 1e12,
+                    "frac_fp32_F_gnn": fs / (gms * 1e-3) / 1e12 / peak, "peak": peak,
                     "subdomain_node_layers_per_s": info["V"] * kb / (gms * 1e-3),
                     "problem_build_s": t_build}), flush=True)
                 del p

@@ -56,7 +56,7 @@ int main() {
   }
   printf("{\"fp32_ffma2_tflops\": %.2f, \"sms\": %d, \"blocks\": %d, \"threads\": %d, "
          "\"nominal_at_max_clock_tflops\": %.2f, \"err\": \"%s\"}\n",
-         best, sms, blocks, threads, sms * 128 * 2 * clk_khz * 1e3 / 1e12,
+         best, sms, blocks, threads, sms * 128.0 * 2.0 * clk_khz * 1e3 / 1e12,
          cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
