@@ -583,7 +583,7 @@ def run_ours(args):
     e2e_value = world / float(e2e_t.item())
 
     # ---- time-to-solution: device-resident PCG to 1e-6 (trained weights) ----
-    pcg = pcg_trained = pcg_flex = tts_small = None
+    pcg = pcg_trained = pcg_flex = fcg_trained = tts_small = None
     if not args.no_pcg:
         pcg = time_to_solution(ddm, p, w.a, w.b, args, lvl, dev, stream)
         pcg_flex = time_to_solution(ddm, p, w.a, w.b, args, lvl, dev, stream, flexible=True)
@@ -592,6 +592,8 @@ def run_ours(args):
             path = os.path.join(ROOT, "weights", cand)
             if os.path.exists(path) and args.subdomain_size == 1000 and args.kbar == 10:
                 pcg_trained = time_to_solution(ddm, p, w.a, w.b, args, lvl, dev, stream, path)
+                fcg_trained = time_to_solution(ddm, p, w.a, w.b, args, lvl, dev, stream, path,
+                                               flexible=True)
                 break
         if world == 1:
             tts_small = gpu_tts_small(ddm, args, dev, stream)
@@ -659,6 +661,7 @@ def run_ours(args):
             "pcg": pcg,
             "pcg_flexible": pcg_flex,
             "pcg_trained_weights": pcg_trained,
+            "pcg_flexible_trained_weights": fcg_trained,
             "time_to_solution_small": tts_small,
             "setup_s": {"problem_load": w.seconds, "preconditioner_build": t_build},
         }

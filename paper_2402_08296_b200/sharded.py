@@ -351,14 +351,26 @@ class PeerArena:
         dist.all_gather_object(everyone, (handle.raw, offsets), group=comm.group)
         self._opened = []
         bases = []
+        err = None
         for h, (hnd, _offs) in enumerate(everyone):
             if h == me:
                 bases.append(self._own)
                 continue
             ptr = ctypes.c_void_p()
-            _lib.check(lib.ddmgnn_ipc_open(self.device, hnd, ctypes.byref(ptr)))
+            try:
+                _lib.check(lib.ddmgnn_ipc_open(self.device, hnd, ctypes.byref(ptr)))
+            except RuntimeError as exc:  # e.g. no peer access between these two GPUs
+                err = f"rank {me} cannot map rank {h}'s buffers: {exc}"
+                break
             self._opened.append(ptr.value)
             bases.append(ptr.value)
+        # every rank must agree, or the ranks would run different exchange modes
+        verdicts = [None] * g
+        dist.all_gather_object(verdicts, err, group=comm.group)
+        bad = [v for v in verdicts if v]
+        if bad:
+            self.close()
+            raise RuntimeError("peer exchange unavailable: " + bad[0])
         self.g, self.me = g, me
         self.offsets = offsets
         self._arr = {}
