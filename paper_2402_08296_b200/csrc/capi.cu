@@ -859,6 +859,11 @@ static int check_status_word(ddmgnn_ctx* c, cudaStream_t s) {
   CUDA_TRY(cudaMemcpyAsync(&c->h_st->pad, c->d_status, sizeof(int), cudaMemcpyDeviceToHost, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   st = c->h_st->pad;
+  if (st == kStagingTimeout) {
+    CUDA_TRY(cudaMemsetAsync(c->d_status, 0, sizeof(int), s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return fail(kCudaError, "input staging timed out (a chunk of r never reached the device)");
+  }
   if (st != 0) {
     CUDA_TRY(cudaMemsetAsync(c->d_status, 0, sizeof(int), s));
     CUDA_TRY(cudaStreamSynchronize(s));
@@ -908,6 +913,9 @@ extern "C" int ddmgnn_apply_host(ddmgnn_ctx* c, const double* r, double* z, int 
     // r in kStages chunks on the copy stream, each followed by its ready flag; the
     // GNN's CTAs (ordered by the chunk they need) start on the first chunk while the
     // rest is still crossing PCIe
+    // the copies and flag writes are enqueued BEFORE the kernels that wait for them:
+    // streams can share hardware queues, so a copy queued behind a spinning kernel
+    // could never start
     const unsigned int ep = ++c->stage_epoch;
     WriteValue32Fn wv = write_value32();
     for (int ci = 0; ci < kStages; ++ci) {

@@ -47,6 +47,7 @@ enum DevStatus : int {
   kNotSpd = 3,
   kNonFiniteResidual = 4,
   kPrecondError = 5,
+  kStagingTimeout = 6,  // ddmgnn_apply_host: an input chunk never arrived (apply word only)
 };
 
 #ifndef GNN_THREADS

@@ -842,10 +842,20 @@ __device__ __forceinline__ void wait_input(const GnnArgs& a, int sub) {
   if (threadIdx.x == 0) {
     const unsigned int* f = a.ready + a.sub_stage[sub];
     unsigned int v;
+    unsigned long long t0 = 0;
     while (true) {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
       if (static_cast<int>(v - a.epoch) >= 0) break;
       __nanosleep(256);
+      // never hang the GPU on a chunk that does not come: give up after ~5 s and
+      // raise the apply's error word (the host reports it; the result is discarded)
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      if (t0 == 0) t0 = t;
+      if (t - t0 > 5000000000ull) {
+        atomicMax(a.status, static_cast<int>(kStagingTimeout));
+        break;
+      }
     }
   }
   __syncthreads();

@@ -109,9 +109,10 @@ __global__ void __launch_bounds__(kSpmvRows) spmv_kernel(SellMatrix m, const dou
                                                          double* __restrict__ y, double* partials,
                                                          PcgState* st) {
   if (PQ && st->status != kRunning) return;
-  const int row = blockIdx.x * kSpmvRows + threadIdx.x;
   double pq = 0.0;
-  if (row < m.n) {
+  // grid-stride over rows with a grid of at most 8 blocks per SM: the fused <p, Ap>
+  // reduction then has <= 1184 block partials instead of one per 256 rows
+  for (int row = blockIdx.x * kSpmvRows + threadIdx.x; row < m.n; row += gridDim.x * kSpmvRows) {
     const int q = row >> 5;
     const int off = __ldg(&m.off[q]);
     const int w = (__ldg(&m.off[q + 1]) - off) >> 5;
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(kSpmvRows) spmv_kernel(SellMatrix m, const dou
         if (c[u] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[u], xv[u]));
     }
     y[row] = acc;
-    if (PQ) pq = x[row] * acc;
+    if (PQ) pq += x[row] * acc;
   }
   if (PQ) {
     double v[1] = {pq};
@@ -152,17 +153,19 @@ __global__ void __launch_bounds__(kSpmvRows) spmv_kernel(SellMatrix m, const dou
   }
 }
 
+static int spmv_blocks(int n) {
+  return std::max(1, std::min((n + kSpmvRows - 1) / kSpmvRows, kMaxRedBlocks));
+}
+
 cudaError_t launch_spmv(const SellMatrix& m, const double* x, double* y, cudaStream_t s) {
   if (m.n <= 0) return cudaSuccess;
-  spmv_kernel<false><<<(m.n + kSpmvRows - 1) / kSpmvRows, kSpmvRows, 0, s>>>(m, x, y, nullptr,
-                                                                           nullptr);
+  spmv_kernel<false><<<spmv_blocks(m.n), kSpmvRows, 0, s>>>(m, x, y, nullptr, nullptr);
   return cudaGetLastError();
 }
 
 cudaError_t launch_spmv_pq(const SellMatrix& m, const double* p, double* q, double* partials,
                            PcgState* st, cudaStream_t s) {
-  spmv_kernel<true><<<(m.n + kSpmvRows - 1) / kSpmvRows, kSpmvRows, 0, s>>>(m, p, q, partials,
-                                                                          st);
+  spmv_kernel<true><<<spmv_blocks(m.n), kSpmvRows, 0, s>>>(m, p, q, partials, st);
   return cudaGetLastError();
 }
 
@@ -404,67 +407,67 @@ cudaError_t launch_copy(int n, const double* src, double* dst, cudaStream_t s) {
 // byte stream in flight; with an even ld (the context pads its copy) every thread
 // issues its 16-byte row loads back to back.  Fixed reduction order.  Replaces
 // the dense LU solve of sparse.py:163 (coarse matrix factorised at setup).
-constexpr int kGemvRowThreads = 128;
+constexpr int kGemvRowThreads = 64;   // two warps per row, four rows per block
+constexpr int kGemvRows = 256 / kGemvRowThreads;
 __global__ void __launch_bounds__(256) coarse_gemv_kernel(int K, int ld,
                                                           const double* __restrict__ inv,
                                                           const double* __restrict__ x,
                                                           double* __restrict__ y,
                                                           const int* skip) {
   if (skip != nullptr && *skip != kRunning) return;
-  __shared__ double part[2][kGemvRowThreads / 32];
-  const int half = threadIdx.x / kGemvRowThreads;  // which of the block's two rows
+  __shared__ double part[kGemvRows][kGemvRowThreads / 32];
+  const int sub = threadIdx.x / kGemvRowThreads;  // which of the block's rows
   const int t = threadIdx.x % kGemvRowThreads;
-  const int row = blockIdx.x * 2 + half;
+  const int row = blockIdx.x * kGemvRows + sub;
   double acc = 0.0;
   if (row < K) {
-    // thread t takes column pairs (2j, 2j+1), j = t, t + 128, ... in this order
+    // thread t takes column pairs (2j, 2j+1), j = t, t + 64, ... in this order
     // whatever the alignment (16-byte loads when possible), so the result does not
-    // depend on ld or on where the matrix lives (sharded solve: bit-identical z)
+    // depend on ld or on where the matrix lives (sharded solve: bit-identical z);
+    // eight pairs per thread are in flight before the first FMA
     const double* rp = inv + static_cast<size_t>(row) * ld;
     const int k2 = K >> 1;
-    if ((ld & 1) == 0 && aligned16(inv) && aligned16(x)) {
-      const double2* r2 = reinterpret_cast<const double2*>(rp);
-      const double2* x2 = reinterpret_cast<const double2*>(x);
-      int j = t;
-      for (; j + 3 * kGemvRowThreads < k2; j += 4 * kGemvRowThreads) {
-        const double2 a0 = __ldcs(r2 + j), a1 = __ldcs(r2 + j + kGemvRowThreads);
-        const double2 a2 = __ldcs(r2 + j + 2 * kGemvRowThreads);
-        const double2 a3 = __ldcs(r2 + j + 3 * kGemvRowThreads);
-        const double2 b0 = __ldg(x2 + j), b1 = __ldg(x2 + j + kGemvRowThreads);
-        const double2 b2 = __ldg(x2 + j + 2 * kGemvRowThreads);
-        const double2 b3 = __ldg(x2 + j + 3 * kGemvRowThreads);
-        acc = fma(a0.x, b0.x, acc); acc = fma(a0.y, b0.y, acc);
-        acc = fma(a1.x, b1.x, acc); acc = fma(a1.y, b1.y, acc);
-        acc = fma(a2.x, b2.x, acc); acc = fma(a2.y, b2.y, acc);
-        acc = fma(a3.x, b3.x, acc); acc = fma(a3.y, b3.y, acc);
+    const bool vec = (ld & 1) == 0 && aligned16(inv) && aligned16(x);
+    for (int j0 = t; j0 < k2; j0 += 8 * kGemvRowThreads) {
+      double2 a[8], b[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = j0 + u * kGemvRowThreads;
+        if (j < k2) {
+          if (vec) {
+            a[u] = __ldcs(reinterpret_cast<const double2*>(rp) + j);
+            b[u] = __ldg(reinterpret_cast<const double2*>(x) + j);
+          } else {
+            a[u] = make_double2(__ldcs(rp + 2 * j), __ldcs(rp + 2 * j + 1));
+            b[u] = make_double2(__ldg(x + 2 * j), __ldg(x + 2 * j + 1));
+          }
+        } else {
+          a[u] = b[u] = make_double2(0.0, 0.0);
+        }
       }
-      for (; j < k2; j += kGemvRowThreads) {
-        const double2 a0 = __ldcs(r2 + j), b0 = __ldg(x2 + j);
-        acc = fma(a0.x, b0.x, acc);
-        acc = fma(a0.y, b0.y, acc);
-      }
-    } else {
-      for (int j = t; j < k2; j += kGemvRowThreads) {
-        acc = fma(__ldcs(rp + 2 * j), __ldg(x + 2 * j), acc);
-        acc = fma(__ldcs(rp + 2 * j + 1), __ldg(x + 2 * j + 1), acc);
-      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (j0 + u * kGemvRowThreads < k2) {
+          acc = fma(a[u].x, b[u].x, acc);
+          acc = fma(a[u].y, b[u].y, acc);
+        }
     }
     if ((K & 1) && t == 0) acc = fma(__ldcs(rp + K - 1), __ldg(x + K - 1), acc);
   }
   acc = warp_sum_d(acc);
-  if ((threadIdx.x & 31) == 0) part[half][t >> 5] = acc;
+  if ((threadIdx.x & 31) == 0) part[sub][t >> 5] = acc;
   __syncthreads();
   if (t == 0 && row < K) {
     double s = 0.0;
 #pragma unroll
-    for (int w = 0; w < kGemvRowThreads / 32; ++w) s += part[half][w];
+    for (int w = 0; w < kGemvRowThreads / 32; ++w) s += part[sub][w];
     y[row] = s;
   }
 }
 
 cudaError_t launch_coarse_gemv(int K, int ld, const double* inv, const double* x, double* y,
                                const int* skip, cudaStream_t s) {
-  coarse_gemv_kernel<<<(K + 1) / 2, 2 * kGemvRowThreads, 0, s>>>(K, ld, inv, x, y, skip);
+  coarse_gemv_kernel<<<(K + kGemvRows - 1) / kGemvRows, 256, 0, s>>>(K, ld, inv, x, y, skip);
   return cudaGetLastError();
 }
 
@@ -542,6 +545,44 @@ __device__ __forceinline__ double glue_dof(int j, int two_level, const int* __re
                                            const double* __restrict__ zloc) {
   const int b = tptr[j], e = tptr[j + 1];
   double acc = 0.0;
+  if (e - b <= 4) {
+    // common case (multiplicity <= 4): every entry's loads issued together — one
+    // round trip for the entries, one for their values — then the same ordered sums
+    int2 te[4];
+    double zl[4], yv[4], sc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) te[u] = b + u < e ? __ldg(tent + b + u) : make_int2(0, 0);
+    const double w = (two_level & 1) ? __ldg(pou + j) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool in = b + u < e;
+      zl[u] = in ? __ldg(zloc + te[u].x) : 0.0;
+      yv[u] = in && (two_level & 1) ? __ldg(y + te[u].y) : 0.0;
+      sc[u] = in && !(two_level & 2) ? __ldg(scale + te[u].y) : 0.0;
+    }
+    if (two_level & 2) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (b + u < e) acc = __dadd_rn(acc, zl[u]);
+      if (two_level & 1) {
+        double c = 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (b + u < e) c = __dadd_rn(c, __dmul_rn(w, yv[u]));
+        acc = __dadd_rn(acc, c);
+      }
+    } else {
+      if (two_level) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (b + u < e) acc = __dadd_rn(acc, __dmul_rn(w, yv[u]));
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (b + u < e && sc[u] != 0.0) acc = __dadd_rn(acc, zl[u]);
+    }
+    return acc;
+  }
   if (two_level & 2) {
     // ASM order (asm.py:108-113): local sum first, coarse correction added last
     for (int t = b; t < e; ++t) acc = __dadd_rn(acc, zloc[tent[t].x]);
