@@ -13,7 +13,8 @@ from paper_2402_08296_b200 import _lib  # noqa: E402
 from paper_2402_08296_b200.problem import ProblemConfig, build_problem  # noqa: E402
 
 target = int(os.environ.get("TARGET_NODES", "1000000"))
-prob = build_problem(0, ProblemConfig(target, 0.2, 1000, 2))
+ns = int(os.environ.get("SUBDOMAIN_SIZE", "1000"))
+prob = build_problem(0, ProblemConfig(target, 0.2, ns, 2))
 p = ddm.build_ddm_gnn(prob.system.a, prob.coords, prob.dec, ddm.init_model(10, 10, seed=1))
 ctx = p.context
 dev = torch.device("cuda:0")
@@ -40,5 +41,5 @@ for i in range(20):
     torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
     tg.append(g0.elapsed_time(g1))
-print(json.dumps({"lib": os.path.basename(_lib.LIB_PATH), "apply_ms": float(np.median(ts)),
+print(json.dumps({"lib": os.path.basename(_lib.LIB_PATH), "N_s": ns, "apply_ms": float(np.median(ts)),
                   "gnn_ms": float(np.median(tg)), "repeat_bitwise": bool(torch.equal(z, ref))}))
