@@ -545,44 +545,6 @@ __device__ __forceinline__ double glue_dof(int j, int two_level, const int* __re
                                            const double* __restrict__ zloc) {
   const int b = tptr[j], e = tptr[j + 1];
   double acc = 0.0;
-  if (e - b <= 4) {
-    // common case (multiplicity <= 4): every entry's loads issued together — one
-    // round trip for the entries, one for their values — then the same ordered sums
-    int2 te[4];
-    double zl[4], yv[4], sc[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) te[u] = b + u < e ? __ldg(tent + b + u) : make_int2(0, 0);
-    const double w = (two_level & 1) ? __ldg(pou + j) : 0.0;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const bool in = b + u < e;
-      zl[u] = in ? __ldg(zloc + te[u].x) : 0.0;
-      yv[u] = in && (two_level & 1) ? __ldg(y + te[u].y) : 0.0;
-      sc[u] = in && !(two_level & 2) ? __ldg(scale + te[u].y) : 0.0;
-    }
-    if (two_level & 2) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (b + u < e) acc = __dadd_rn(acc, zl[u]);
-      if (two_level & 1) {
-        double c = 0.0;
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (b + u < e) c = __dadd_rn(c, __dmul_rn(w, yv[u]));
-        acc = __dadd_rn(acc, c);
-      }
-    } else {
-      if (two_level) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (b + u < e) acc = __dadd_rn(acc, __dmul_rn(w, yv[u]));
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (b + u < e && sc[u] != 0.0) acc = __dadd_rn(acc, zl[u]);
-    }
-    return acc;
-  }
   if (two_level & 2) {
     // ASM order (asm.py:108-113): local sum first, coarse correction added last
     for (int t = b; t < e; ++t) acc = __dadd_rn(acc, zloc[tent[t].x]);
