@@ -774,8 +774,9 @@ def run_sharded(args, world, rank, local):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32 GNN / f64 Krylov+gluing",
             "data": "synthetic (reference problem generator restated natively; random-init weights)",
-            "config": dict(config_obj(args, w, world), exchange=exchange,
-                           graph=graph is not None),
+            "config": config_obj(args, w, world),
+            "sharding": {"exchange": exchange, "graph": graph is not None,
+                         "ranks": world},
             "e2e": {"value": 1.0 / float(e2e.item()), "unit": UNIT,
                     "h2d_bytes_per_step": 8 * sh.plan.n_own, "d2h_bytes_per_step": 8 * sh.plan.n_own},
             "gpu_launches": sh.launches_per_apply() * args.steps, "clocks": clk.summary(),
