@@ -61,6 +61,14 @@ constexpr int kFlatWarps = 8;        // slices (warps) per CTA of the flat path
 // pipe (0); the bank's message weights carry the matching factor (layout.cpp)
 #define GNN_EDGE_RELU_MAX 1
 #endif
+#ifndef GNN_EDGE_SHIFT
+// edge loop as sum_e max(Q_t + |d| WL, -P) + width P (= sum_e relu(P + Q_t + |d| WL)):
+// 2 instead of 3 packed FMA-pipe ops per pair and edge (gnn_impl.cuh slice_u)
+#define GNN_EDGE_SHIFT 1
+#endif
+#if GNN_EDGE_SHIFT && !GNN_EDGE_RELU_MAX
+#error "GNN_EDGE_SHIFT sums relu(x) (not 2 relu(x)): it needs GNN_EDGE_RELU_MAX=1"
+#endif
 #ifndef GNN_Q2
 #define GNN_Q2 1  // phase A two slices per warp (shared weight loads; 2.4% faster)
 #endif

@@ -48,6 +48,12 @@ __device__ __forceinline__ float relu_nan(float x) {
   return y;
 }
 
+__device__ __forceinline__ float max_nan(float x, float y) {
+  float z;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(z) : "f"(x), "f"(y));
+  return z;
+}
+
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 __device__ __forceinline__ float2 fadd2(float2 a, float2 b) { return __fadd2_rn(a, b); }
 __device__ __forceinline__ float2 bcast(float x) { return make_float2(x, x); }
@@ -265,6 +271,15 @@ __device__ __forceinline__ bool slice_u(int n0, int k, float* h, Rows q,
     const float2 len = bcast(cur.x);
 #pragma unroll
     for (int j = 0; j < NP2; ++j) {
+#if GNN_EDGE_SHIFT
+      // relu(P + y) = max(y, -P) + P with y = Q_t + |d| WL: the P of every edge is
+      // added once after the loop (width P; a padding record's y = -1e30 gives
+      // max = -P, so it contributes exactly nothing), which leaves 2 of the 3 packed
+      // FMA-pipe ops per pair and edge; max.NaN propagates NaN like numpy.maximum
+      const float2 y = ffma2(len, cpair(W + C::OFF_WL + 2 * j),
+                             make_float2(qt[2 * j], qt[2 * j + 1]));
+      s[j] = fadd2(s[j], make_float2(max_nan(y.x, -p[j].x), max_nan(y.y, -p[j].y)));
+#else
       float2 x = fadd2(p[j], make_float2(qt[2 * j], qt[2 * j + 1]));
       x = ffma2(len, cpair(W + C::OFF_WL + 2 * j), x);
 #if GNN_EDGE_RELU_MAX
@@ -274,8 +289,16 @@ __device__ __forceinline__ bool slice_u(int n0, int k, float* h, Rows q,
 #else
       s[j] = fadd2(s[j], relu2x(x));
 #endif
+#endif
     }
   }
+#if GNN_EDGE_SHIFT
+  {
+    const float2 wdt = bcast(static_cast<float>(width));
+#pragma unroll
+    for (int j = 0; j < NP2; ++j) s[j] = ffma2(wdt, p[j], s[j]);
+  }
+#endif
   // psi first layer with the messages' second layer folded in; the message part
   // accumulates in a second, independent chain (ILP)
   float2 u[NPH], u2[NPH];
