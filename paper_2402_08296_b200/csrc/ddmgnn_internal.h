@@ -66,6 +66,9 @@ constexpr int kFlatWarps = 8;        // slices (warps) per CTA of the flat path
 // 2 instead of 3 packed FMA-pipe ops per pair and edge (gnn_impl.cuh slice_u)
 #define GNN_EDGE_SHIFT 1
 #endif
+#ifndef GNN_EDGE_PREFETCH
+#define GNN_EDGE_PREFETCH 1  // L1 prefetch of a slice's edge records before its P mat-vec
+#endif
 #if GNN_EDGE_SHIFT && !GNN_EDGE_RELU_MAX
 #error "GNN_EDGE_SHIFT sums relu(x) (not 2 relu(x)): it needs GNN_EDGE_RELU_MAX=1"
 #endif

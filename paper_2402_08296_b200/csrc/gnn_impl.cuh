@@ -241,6 +241,17 @@ __device__ __forceinline__ bool slice_u(int n0, int k, float* h, Rows q,
   const int lane = threadIdx.x & 31;
   const int n = n0 + lane;
   const int nn = min(n, k - 1);
+#if GNN_EDGE_PREFETCH
+  // the slice's edge records (width rows of 32 x 8 B) are re-read from L2 in every
+  // layer (they do not fit L1 next to the node state): ask for them now, one
+  // 128-byte line per lane, so the edge loop below finds them in L1 after the P
+  // mat-vec instead of waiting on L2 one record ahead
+  {
+    const char* line = reinterpret_cast<const char*>(edges + so) + 128 * lane;
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %1, %2;\n\t@p prefetch.global.L1 [%0];\n\t}"
+                 ::"l"(line), "r"(lane), "r"(2 * width));
+  }
+#endif
   float2 p[NP2], s[NP2];
   {
     float hin[D + 2];
