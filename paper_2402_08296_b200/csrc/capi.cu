@@ -207,7 +207,7 @@ static void free_graphs(ddmgnn_ctx* c) {
 static void free_layout(ddmgnn_ctx* c) {
   DeviceLayout& L = c->lay;
   dfree(L.sub_ptr); dfree(L.idx); dfree(L.order); dfree(L.slice_base); dfree(L.slice_off);
-  dfree(L.deg); dfree(L.edges); dfree(L.xy); dfree(L.tptr); dfree(L.tent); dfree(L.pou);
+  dfree(L.reach); dfree(L.deg); dfree(L.edges); dfree(L.xy); dfree(L.tptr); dfree(L.tent); dfree(L.pou);
   dfree(c->d_r0r); dfree(c->d_scale); dfree(c->d_zloc); dfree(c->d_y);
   dfree(c->d_bad); dfree(c->d_outbad);
   dfree(c->d_hbuf); dfree(c->d_cbuf); dfree(c->d_qbuf); dfree(c->d_bslices); dfree(c->d_csubs);
@@ -574,6 +574,7 @@ extern "C" int ddmgnn_build(ddmgnn_ctx* c) {
   CUDA_TRY(upload(&L.order, H.order));
   CUDA_TRY(upload(&L.slice_base, H.slice_base));
   CUDA_TRY(upload(&L.slice_off, H.slice_off));
+  CUDA_TRY(upload(&L.reach, H.reach));
   CUDA_TRY(upload(&L.deg, H.deg));
   CUDA_TRY(dalloc(&L.edges, std::max<long long>(H.E_pad, 1)));
   if (H.E_pad)
@@ -736,7 +737,11 @@ static cudaError_t enqueue_gnn_impl(ddmgnn_ctx* c, const double* r, int* status,
   const PackedModel& M = c->model;
   GnnArgs a{};
   a.sub_ptr = L.sub_ptr; a.idx = L.idx; a.order = L.order; a.slice_base = L.slice_base;
-  a.slice_off = L.slice_off; a.deg = L.deg; a.edges = L.edges; a.xy = L.xy; a.pou = L.pou;
+  a.slice_off = L.slice_off; a.deg = L.deg;
+  {  // DDMGNN_DATAFLOW=0: two CTA barriers per layer (the schedule before round 2's end)
+    const char* df = getenv("DDMGNN_DATAFLOW");
+    a.reach = (df && df[0] == '0') ? nullptr : L.reach;
+  } a.edges = L.edges; a.xy = L.xy; a.pou = L.pou;
   a.r = r; a.r0r = c->d_r0r; a.scale = c->d_scale; a.zloc = c->d_zloc;
   a.hbuf = c->d_hbuf; a.cbuf = c->d_cbuf; a.qbuf = c->d_qbuf;
   a.bslices = c->d_bslices; a.n_bslices = c->n_bslices;

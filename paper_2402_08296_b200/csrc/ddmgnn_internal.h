@@ -69,6 +69,14 @@ constexpr int kFlatWarps = 8;        // slices (warps) per CTA of the flat path
 #ifndef GNN_EDGE_PREFETCH
 #define GNN_EDGE_PREFETCH 1  // L1 prefetch of a slice's edge records before its P mat-vec
 #endif
+#ifndef GNN_DATAFLOW
+// CTA path: layers as a dataflow over slices (per-slice phase flags in shared
+// memory, dependencies within the subdomain's slice reach) instead of two CTA
+// barriers per layer (gnn_impl.cuh cta_layer_df)
+#define GNN_DATAFLOW 1
+#endif
+constexpr int kDfMaxSlices = 64;  // per-slice flags in GnnShared (k <= 2048)
+constexpr int kDfMaxReach = 15;   // 2 R + 2 <= 32 flags polled by one warp
 #if GNN_EDGE_SHIFT && !GNN_EDGE_RELU_MAX
 #error "GNN_EDGE_SHIFT sums relu(x) (not 2 relu(x)): it needs GNN_EDGE_RELU_MAX=1"
 #endif
@@ -88,6 +96,7 @@ struct DeviceLayout {
   long long E = 0, E_pad = 0;
   int *sub_ptr = nullptr, *idx = nullptr, *order = nullptr;
   int *slice_base = nullptr, *slice_off = nullptr;
+  int* reach = nullptr;  // per subdomain: max |slice(dst) - slice(src)| over its edges
   uint16_t* deg = nullptr;
   float2* edges = nullptr;
   float2* xy = nullptr;
@@ -102,6 +111,7 @@ struct HostLayout {
   int n = 0, K = 0, V = 0, S = 0, k_max = 0;
   long long E = 0, E_pad = 0;
   std::vector<int> sub_ptr, idx, order, slice_base, slice_off;
+  std::vector<int> reach;  // per subdomain: max |slice(dst) - slice(src)| over its edges
   std::vector<uint16_t> deg;
   std::vector<float> edges;  // 2 floats per record
   std::vector<float> xy;     // 2 floats per batched node
@@ -139,6 +149,7 @@ struct GnnArgs {
   const int* order;
   const int* slice_base;
   const int* slice_off;
+  const int* reach;  // per subdomain slice reach (dataflow layer schedule; null = barriers)
   const uint16_t* deg;
   const float2* edges;
   const float2* xy;

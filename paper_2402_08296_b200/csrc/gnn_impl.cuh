@@ -855,6 +855,72 @@ __device__ __forceinline__ void cta_layer(const SmemState<D>& ns, int k, int war
   __syncthreads();
 }
 
+// ---- dataflow schedule of the CTA path (GNN_DATAFLOW) -----------------------------
+// The two CTA barriers per layer leave warps idle whenever a phase has fewer slices
+// left than warps (config C: 34-61 slices over 28 warps).  A slice's edges reach at
+// most R slices away (the subdomain's DOF order is banded; layout.cpp measures R), so
+// the dependencies are local:
+//   A(l, s)  overwrites Q rows of s: every B(l-1, s') with |s' - s| <= R has read them
+//   B(l, s)  reads the Q rows of slices s-R..s+R: A(l, s') done for |s' - s| <= R
+// Work items (A pairs of adjacent slices, then B slices, layer after layer) are dealt
+// round robin over the warps as ONE sequence, so the assignment rotates from layer to
+// layer and the load balances over the whole chunk instead of within each phase.  An
+// item only waits for items earlier in the sequence, each warp takes its items in
+// sequence order, so the earliest unfinished item is always ready: no deadlock.
+// flags: fa[s] = layers whose phase A wrote s, fb[s] = layers whose phase B updated s.
+__device__ __forceinline__ void df_wait(const int* f, int lo, int hi, int nsl, int need) {
+  lo = max(lo, 0);
+  hi = min(hi, nsl - 1);
+  const int s = lo + static_cast<int>(threadIdx.x & 31);
+  const volatile int* vf = f;
+  while (true) {
+    const int v = s <= hi ? vf[s] : need;
+    if (__all_sync(0xffffffffu, v >= need)) break;
+    __nanosleep(20);
+  }
+  asm volatile("fence.acq_rel.cta;" ::: "memory");  // acquire: rows written before the flags
+}
+
+__device__ __forceinline__ void df_post(int* f, int s1, int s2, int val) {
+  asm volatile("fence.acq_rel.cta;" ::: "memory");  // release: this warp's rows before the flag
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) {
+    volatile int* vf = f;
+    vf[s1] = val;
+    vf[s2] = val;
+  }
+}
+
+template <int D, int W, bool H0 = false>
+__device__ __forceinline__ void cta_layer_df(const SmemState<D>& ns, int k, int warp, int nw,
+                                             const float2* xy, const float2* edges,
+                                             const int* slice_off, const uint16_t* deg,
+                                             float alpha, int* bad, int layer_no, int ll,
+                                             int reach, int (&df)[2][kDfMaxSlices], int& t0) {
+  const int nsl = (k + 31) >> 5, npairs = (nsl + 1) >> 1;
+  // phase A: pairs (2j, 2j + 1) (odd count: the last pair repeats its slice)
+  for (int j = (warp - t0 % nw + nw) % nw; j < npairs; j += nw) {
+    const int s1 = 2 * j, s2 = min(2 * j + 1, nsl - 1);
+    df_wait(df[1], s1 - reach, s2 + reach, nsl, ll);
+    slice_q2<D, W, H0>(s1 * 32, s2 * 32, k, ns.h, ns.q, xy);
+    df_post(df[0], s1, s2, ll + 1);
+  }
+  t0 += npairs;
+  int first_bad = 0;
+  for (int sl = (warp - t0 % nw + nw) % nw; sl < nsl; sl += nw) {
+    df_wait(df[0], sl - reach, sl + reach, nsl, ll + 1);
+    const int so = uni(slice_off[sl]);
+    const int width = (uni(slice_off[sl + 1]) - so) >> 5;
+    float hn[Cfg<D>::DH];
+    const bool b = slice_u<D, W, LocalRows, H0>(sl * 32, k, ns.h, LocalRows{ns.q}, ns.c, xy, edges,
+                                                so, width, deg, alpha, hn);
+    if (b && first_bad == 0) first_bad = layer_no;
+    df_post(df[1], sl, sl, ll + 1);
+  }
+  t0 += nsl;
+  if (first_bad != 0) atomicCAS(bad, 0, first_bad);  // first bad layer wins
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -863,6 +929,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 struct GnnShared {
   double red[2][kGnnThreads / 32];
+  int df[2][kDfMaxSlices];  // dataflow schedule: layers done per slice, phase A / phase B
   int bad;
   double scale;
   uint64_t mbar[kGnnThreads / 128];  // tensor-core groups (GNN_TC_Q)
@@ -986,6 +1053,11 @@ __global__ void __launch_bounds__(gnn_cta_threads<D>(), 1) gnn_kernel(GnnArgs a)
     }
   }
   for (int j = tid; j < C::QS; j += nthr) ns.q[static_cast<size_t>(k) * C::QS + j] = -1e30f;
+#if GNN_DATAFLOW && !GNN_TC_Q
+  const int reach = a.reach != nullptr ? uni(a.reach[sub]) : -1;
+  const bool dflow = reach >= 0 && reach <= kDfMaxReach && ((k + 31) >> 5) <= kDfMaxSlices;
+  for (int i = tid; i < 2 * kDfMaxSlices; i += nthr) (&sh.df[0][0])[i] = 0;
+#endif
   __syncthreads();
   uint32_t tmem = 0, uses = 0;
 #if GNN_TC_Q
@@ -1013,6 +1085,30 @@ __global__ void __launch_bounds__(gnn_cta_threads<D>(), 1) gnn_kernel(GnnArgs a)
       cta_layer<D, LL * C::STRIDE>(ns, k, warp, xy, a.edges, so, dg, a.alpha, &sh.bad,       \
                                    a.layer0 + LL, tmem, sh.mbar, uses);                      \
   }
+#if GNN_DATAFLOW && !GNN_TC_Q
+    if (dflow) {
+      const int nw = uni(nthr >> 5);
+      int t0 = 0;
+#define DDM_LAYER_DF(LL)                                                                     \
+  if constexpr (LL < C::LMAX) {                                                              \
+    if (LL < a.nl)                                                                           \
+      cta_layer_df<D, LL * C::STRIDE>(ns, k, warp, nw, xy, a.edges, so, dg, a.alpha, &sh.bad, \
+                                      a.layer0 + LL, LL, reach, sh.df, t0);                  \
+  }
+      if (a.first && a.h0_skip) {
+        if (a.nl > 0)
+          cta_layer_df<D, 0, true>(ns, k, warp, nw, xy, a.edges, so, dg, a.alpha, &sh.bad,
+                                   a.layer0, 0, reach, sh.df, t0);
+      } else {
+        DDM_LAYER_DF(0)
+      }
+      DDM_LAYER_DF(1) DDM_LAYER_DF(2) DDM_LAYER_DF(3) DDM_LAYER_DF(4)
+      DDM_LAYER_DF(5) DDM_LAYER_DF(6) DDM_LAYER_DF(7) DDM_LAYER_DF(8) DDM_LAYER_DF(9)
+#undef DDM_LAYER_DF
+      __syncthreads();
+    } else
+#endif
+    {
 #if !GNN_TC_Q
     // the first layer of the model starts from h = 0 (dss.py:309)
     if (a.first && a.h0_skip) {
@@ -1027,6 +1123,7 @@ __global__ void __launch_bounds__(gnn_cta_threads<D>(), 1) gnn_kernel(GnnArgs a)
 #endif
     DDM_LAYER(1) DDM_LAYER(2) DDM_LAYER(3) DDM_LAYER(4)
     DDM_LAYER(5) DDM_LAYER(6) DDM_LAYER(7) DDM_LAYER(8) DDM_LAYER(9)
+    }
 #undef DDM_LAYER
   }
 #if GNN_TC_Q

@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -137,6 +138,7 @@ int build_host_layout(int n, const int64_t* indptr, const int32_t* indices, cons
   L.E = E;
   L.E_pad = off;
   L.edges.assign(static_cast<size_t>(off) * 2, 0.f);
+  L.reach.assign(K, 0);
   L.xy.assign(2ull * L.V, 0.f);
 
   // ---- pass 2: edge records {|d|, dst} (dss.py:177-185) and centred coordinates ----
@@ -170,6 +172,7 @@ int build_host_layout(int n, const int64_t* indptr, const int32_t* indices, cons
           std::memcpy(&L.edges[2 * r + 1], &kk, 4);
         }
       }
+      int reach = 0;
       for (int p = b; p < e; ++p) {
         const int a = p - b, g = L.idx[p];
         L.xy[2ull * p] = static_cast<float>(coords[2 * g] - cx);
@@ -185,9 +188,11 @@ int build_host_layout(int n, const int64_t* indptr, const int32_t* indices, cons
           rec[0] = static_cast<float>(std::hypot(dx, dy));
           int dst = loc[c];
           std::memcpy(&rec[1], &dst, 4);
+          reach = std::max(reach, std::abs((dst >> 5) - (a >> 5)));
           ++slot;
         }
       }
+      L.reach[i] = reach;
       for (int p = b; p < e; ++p) loc[L.idx[p]] = -1;
     }
   }
