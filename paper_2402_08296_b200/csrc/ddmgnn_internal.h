@@ -75,6 +75,12 @@ constexpr int kFlatWarps = 8;        // slices (warps) per CTA of the flat path
 // barriers per layer (gnn_impl.cuh cta_layer_df)
 #define GNN_DATAFLOW 1
 #endif
+#ifndef GNN_DF_SLEEP
+#define GNN_DF_SLEEP 20  // ns between polls of a dataflow wait
+#endif
+#ifndef GNN_DF_PAIRS
+#define GNN_DF_PAIRS 1  // phase-A items are pairs of adjacent slices (shared weight loads)
+#endif
 constexpr int kDfMaxSlices = 64;  // per-slice flags in GnnShared (k <= 2048)
 constexpr int kDfMaxReach = 15;   // 2 R + 2 <= 32 flags polled by one warp
 #if GNN_EDGE_SHIFT && !GNN_EDGE_RELU_MAX

@@ -876,7 +876,7 @@ __device__ __forceinline__ void df_wait(const int* f, int lo, int hi, int nsl, i
   while (true) {
     const int v = s <= hi ? vf[s] : need;
     if (__all_sync(0xffffffffu, v >= need)) break;
-    __nanosleep(20);
+    __nanosleep(GNN_DF_SLEEP);
   }
   asm volatile("fence.acq_rel.cta;" ::: "memory");  // acquire: rows written before the flags
 }
@@ -897,8 +897,10 @@ __device__ __forceinline__ void cta_layer_df(const SmemState<D>& ns, int k, int 
                                              const int* slice_off, const uint16_t* deg,
                                              float alpha, int* bad, int layer_no, int ll,
                                              int reach, int (&df)[2][kDfMaxSlices], int& t0) {
-  const int nsl = (k + 31) >> 5, npairs = (nsl + 1) >> 1;
+  const int nsl = (k + 31) >> 5;
+#if GNN_DF_PAIRS
   // phase A: pairs (2j, 2j + 1) (odd count: the last pair repeats its slice)
+  const int npairs = (nsl + 1) >> 1;
   for (int j = (warp - t0 % nw + nw) % nw; j < npairs; j += nw) {
     const int s1 = 2 * j, s2 = min(2 * j + 1, nsl - 1);
     df_wait(df[1], s1 - reach, s2 + reach, nsl, ll);
@@ -906,6 +908,16 @@ __device__ __forceinline__ void cta_layer_df(const SmemState<D>& ns, int k, int 
     df_post(df[0], s1, s2, ll + 1);
   }
   t0 += npairs;
+#else
+  // phase A one slice per item: A(l, s) sits nsl positions after B(l-1, s) in the
+  // item sequence, as B(l, s) after A(l, s), so every dependency is >= nsl - R items back
+  for (int sl = (warp - t0 % nw + nw) % nw; sl < nsl; sl += nw) {
+    df_wait(df[1], sl - reach, sl + reach, nsl, ll);
+    slice_q<D, W>(sl * 32, k, ns.h, ns.q, xy);
+    df_post(df[0], sl, sl, ll + 1);
+  }
+  t0 += nsl;
+#endif
   int first_bad = 0;
   for (int sl = (warp - t0 % nw + nw) % nw; sl < nsl; sl += nw) {
     df_wait(df[0], sl - reach, sl + reach, nsl, ll + 1);

@@ -97,6 +97,13 @@ def gnn_capture(rep_name, out_name):
 
 
 if __name__ == "__main__":
+    if sys.argv[1:] == ["final"]:  # end of round 2: the dataflow kernel (tools/cycle26.sh)
+        launches("r02f_pcg_launches.csv", "r02_pcg_iteration_launches_final.csv")
+        launches("r02f_bench_launches.csv", "r02_bench_launches_final.csv")
+        gnn_capture("r02_gnn_shift.ncu-rep", "r02_gnn_kernel_metrics_shift_barriers.json")
+        print(json.dumps(gnn_capture("r02f_gnn.ncu-rep", "r02_gnn_kernel_metrics_dataflow.json"),
+                         indent=1))
+        sys.exit(0)
     launches("r02_pcg_launches_c3.csv", "r02_pcg_iteration_launches.csv")
     launches("r02_pcg_launches_fused.csv", "r02_pcg_iteration_launches_fused_tail.csv")
     launches("r02_pcg_launches.csv", "r02_pcg_iteration_launches_start.csv")
