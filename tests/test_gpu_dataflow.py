@@ -33,7 +33,10 @@ def _applies(p, r, n, dataflow):
 
 
 @pytest.mark.parametrize("target,ns,level", [(100_000, 1000, "two"), (100_000, 500, "one"),
-                                             (1_000_000, 1000, "two")])
+                                             (1_000_000, 1000, "two"),
+                                             # cluster path (keeps cluster barriers: the
+                                             # switch must not change it)
+                                             (200_000, 2000, "two"), (250_000, 5000, "one")])
 def test_dataflow_schedule_bitwise_equals_barriers(target, ns, level):
     import torch
 

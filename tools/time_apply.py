@@ -14,8 +14,8 @@ from paper_2402_08296_b200.problem import ProblemConfig, build_problem  # noqa: 
 
 target = int(os.environ.get("TARGET_NODES", "1000000"))
 ns = int(os.environ.get("SUBDOMAIN_SIZE", "1000"))
-prob = build_problem(0, ProblemConfig(target, 0.2, ns, 2))
-p = ddm.build_ddm_gnn(prob.system.a, prob.coords, prob.dec, ddm.init_model(10, 10, seed=1))
+prob = build_problem(0, ProblemConfig(target, 0.2, ns, int(os.environ.get("OVERLAP", "2"))))
+p = ddm.build_ddm_gnn(prob.system.a, prob.coords, prob.dec, ddm.init_model(int(os.environ.get("KBAR", "10")), 10, seed=1))
 ctx = p.context
 dev = torch.device("cuda:0")
 st = torch.cuda.Stream()
