@@ -76,12 +76,14 @@ def gnn_flops(k_bar, d, v, e):
 def gnn_flops_exec(k_bar, d, v, e, h0_skip=False):
     """FP32 flops the fused kernel executes (FMA = 2, relu not counted):
     per node and layer Q and P ((d+2) -> 2d each), psi first layer ((3d+2) -> d with the
-    messages' second layer folded in), psi second layer (d -> d), h update (d);
-    per edge and layer P+Q add, |d| FMA, sum add over 2d hidden units; decoder once.
+    messages' second layer folded in), psi second layer (d -> d), h update (d), and the
+    shift-form edge loop's width * P FMA (2d); per edge and layer y = Q + |d| WL (FMA)
+    and the sum add over 2d hidden units (the max is not counted); decoder once.
     With h0_skip the first layer skips the h rows of P, Q and psi (h = 0)."""
     dh = (d + 1) // 2 * 2
-    per_node = 2 * (2 * (d + 2) * 2 * d) + 2 * (3 * d + 2) * dh + 2 * d * dh + 2 * dh
-    per_edge = 2 * d * (1 + 2 + 1)
+    per_node = (2 * (2 * (d + 2) * 2 * d) + 2 * (3 * d + 2) * dh + 2 * d * dh + 2 * dh
+                + 2 * 2 * d)
+    per_edge = 2 * d * (2 + 1)
     skipped = (2 * (2 * d * 2 * d) + 2 * d * dh) * v if h0_skip else 0
     return float(k_bar * (per_node * v + per_edge * e) + (2 * d * dh + 2 * d) * v - skipped)
 
@@ -641,7 +643,7 @@ def run_ours(args):
                 "executed_flops": flops_exec,
                 "executed_tflops": achieved_exec,
                 "frac_executed": achieved_exec / fp32_peak,
-                "executed_note": "FP32 flops the kernel actually issues: k(1820 V + 80 E) + 220 V"
+                "executed_note": "FP32 flops the kernel actually issues: k(1860 V + 60 E) + 220 V"
                                  + (" - 1000 V (layer 1 on h = 0)" if h0 else "")
                                  + " at d=10 (FMA = 2, relu not counted; DESIGN.md §4)",
                 "peak_source": fp32_src,
