@@ -1069,7 +1069,8 @@ __global__ void __launch_bounds__(gnn_cta_threads<D>(), 1) gnn_kernel(GnnArgs a)
   const int reach = a.reach != nullptr ? uni(a.reach[sub]) : -1;
   // only for a full-size CTA with more slices than warps: with fewer slices every
   // phase is one round anyway, and next to a second CTA on the SM (two-CTA mode) the
-  // polling warps measured 1.9x slower than the barriers (r02_exp_dataflow_cluster_twocta)
+  // dataflow CTAs measured 1.9x slower than barrier CTAs (cause open; a poll back-off
+  // did not change it: profiles/r02_exp_dataflow_{cluster_twocta,backoff_twocta})
   const bool dflow = reach >= 0 && reach <= kDfMaxReach && ((k + 31) >> 5) <= kDfMaxSlices &&
                      nthr == gnn_cta_threads<D>() && ((k + 31) >> 5) > (nthr >> 5);
   for (int i = tid; i < 2 * kDfMaxSlices; i += nthr) (&sh.df[0][0])[i] = 0;
